@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""Benchmark: coined Grover walk on a 2-D torus, arc-amplitude updates/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload (BASELINE.json configs[1], "2D Lattice ... (4M vertices, 16M arcs),
+1000 steps"; the vertex/arc counts are those of 2048 x 2048):
+grid(2048, 2048) torus, flip-flop shift, Grover coin, dense random psi0
+(seed 0).  One bench step = 1000 coined-walk steps.  Each GPU holds the full
+2048^2 lattice (weak scaling: N GPUs run N independent lattices — the path
+shards into independent lattices with no data-path collective); the
+whole-job value is the sum over ranks, timed as the max over ranks.
+
+JSON line keys beyond the base contract:
+  roofline      dominant kernel (lattice_step_kernel): 32 B/arc algorithmic,
+                CUDA-event time per launch over the timed region, against the
+                measured HBM copy peak (MEASURED_PEAKS.json)
+  cpu_baseline  the reference algorithm (oracle/ numpy port of backend._csr_rows
+                with the reference's row-block thread pool) on this host
+  e2e           the public API call coined.simulate(engine, spec, (1000,1001,1),
+                psi0) with host (pinned) psi0 in and the host result out
+  also          secondary measurements: 4096^2 (C3 size, the north-star 70 %
+                gate) and the device CSR SpMV path (K1) at 2048^2
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "arc-amplitude updates/sec per coined-walk step (2D lattice); % of HBM roofline"
+UNIT = "arc-updates/s"
+BYTES_PER_ARC = 32          # read psi 16 B + write psi' 16 B
+FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback
+SPEC_HBM_GBS = 8000.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--nx", type=int, default=2048)
+    ap.add_argument("--walk-steps", type=int, default=1000)
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def traffic_per_launch(workload: str):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(p)).get(workload)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-i",
+                 str(self.device), "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(self.NAMES, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def init_dist(world, backend):
+    import torch.distributed as dist
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend)
+    return dist if world > 1 else None
+
+
+def max_over_ranks(x: float, dist, device=None) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm (oracle port of the reference algorithm)
+# ---------------------------------------------------------------------------
+
+def cpu_reference(nx: int, sample_steps: int, threads: int):
+    """Time backend._csr_rows-style CSR steps (reference algorithm, numpy) on
+    the host cores with the reference's row-block thread pool."""
+    from oracle import qwalk_oracle as O
+    offs, cols = O.grid_adjacency(nx, nx)
+    u = O.evolution_operator(offs, cols)
+    rng = np.random.default_rng(0)
+    x = rng.normal(size=u.n_rows) + 1j * rng.normal(size=u.n_rows)
+    x /= np.linalg.norm(x)
+    mv = O.Matvec(threads)
+    mv(u, x)  # warm-up
+    times = []
+    for _ in range(sample_steps):
+        t0 = time.perf_counter()
+        x = mv(u, x)
+        times.append(time.perf_counter() - t0)
+    mv.close()
+    total = sum(times)
+    return {"value": u.n_rows * sample_steps / total, "unit": UNIT, "cores": threads,
+            "kind": "port",
+            "sample": f"{sample_steps} coined steps of grid {nx}x{nx} ({u.n_rows} arcs), numpy CSR "
+                      f"matvec (oracle/ port of backend._csr_rows + row-block pool), "
+                      f"median step {statistics.median(times) * 1e3:.1f} ms, min {min(times) * 1e3:.1f} ms"}
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    nx = args.nx
+    from oracle import qwalk_oracle as O
+    offs, cols = O.grid_adjacency(nx, nx)
+    u = O.evolution_operator(offs, cols)
+    rng = np.random.default_rng(0)
+    x = rng.normal(size=u.n_rows) + 1j * rng.normal(size=u.n_rows)
+    x /= np.linalg.norm(x)
+    mv = O.Matvec(threads)
+    sample = 2   # coined steps per bench step (bounded sample of the 1000)
+    for _ in range(args.warmup):
+        for _ in range(sample):
+            x = mv(u, x)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for _ in range(sample):
+            x = mv(u, x)
+    el = time.perf_counter() - t0
+    mv.close()
+    value = u.n_rows * sample * args.steps / el
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"grid {nx}x{nx} torus flip-flop Grover (C2), reference CPU algorithm",
+                   "arcs": u.n_rows, "coined_steps_per_bench_step": sample, "parallelism": f"{threads} threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{sample} coined steps per bench step of grid {nx}x{nx}; numpy CSR "
+                                   "matvec restating backend._csr_rows with the reference's row-block pool"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+def run_b200(args):
+    import torch
+    import paper_2406_08186_b200 as q
+    from paper_2406_08186_b200 import coined as CO
+
+    rank, world, local = dist_env()
+    if world != args.gpus and world > 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dist = init_dist(world, "nccl")
+    dev = torch.device("cuda", local)
+    eng = q.init_engine("b200", device=local)
+
+    nx = args.nx
+    g = q.graphs.grid(nx, nx)
+    spec = q.CoinedSpec(g)
+    arcs = g.num_arcs
+    walk = args.walk_steps
+    rng = np.random.default_rng(0 + rank)
+    psi = rng.normal(size=arcs) + 1j * rng.normal(size=arcs)
+    psi /= np.linalg.norm(psi)
+    basis = q.graphs.arc_basis(g)
+    psi0 = q.WalkState(basis, psi)
+
+    # ---- device-resident timed region: runner.advance(walk) per bench step
+    runner = CO._LatticeRunner(eng, spec)
+    x = torch.from_numpy(psi0.amplitudes).to(dev)
+    runner.load(x)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        runner.advance(walk)
+    torch.cuda.synchronize(dev)
+    clocks = Clocks(local)
+    clocks.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        runner.advance(walk)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    el_ms = e0.elapsed_time(e1)
+    el_ms = max_over_ranks(el_ms, dist, dev)
+    launches = args.steps * walk
+    per_launch_s = el_ms / 1e3 / launches
+    value = world * arcs * walk * args.steps / (el_ms / 1e3)
+
+    peak, peak_src = peaks()
+    achieved_gbs = BYTES_PER_ARC * arcs / per_launch_s / 1e9
+    workload = f"grid{nx}_flipflop_grover"
+    traffic = traffic_per_launch(workload)
+
+    # ---- e2e: public API with host buffers, H2D + D2H inside the timed region
+    e2e_times = []
+    out_state = None
+    for i in range(1 + args.steps):
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        out_state = CO.simulate(eng, spec, (walk, walk + 1, 1), psi0)[0]
+        torch.cuda.synchronize(dev)
+        t1 = time.perf_counter()
+        if i > 0:
+            e2e_times.append(t1 - t0)
+    e2e_s = max_over_ranks(sum(e2e_times), dist, dev)
+    e2e_value = world * arcs * walk * len(e2e_times) / e2e_s
+    assert abs(out_state.norm() - 1.0) < 1e-9
+
+    extras = {}
+    if not args.no_extras and rank == 0:
+        extras = measure_extras(q, CO, eng, dev, peak)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_reference(nx, 8, os.cpu_count() or 1)
+        except Exception as e:  # pragma: no cover - reported, not fatal
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"failed: {e!r}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": el_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": f"C2: grid {nx}x{nx} torus ({nx * nx} vertices, {arcs} arcs; BASELINE configs[1] "
+                            f"'4M vertices, 16M arcs' per SURVEY D1), flip-flop Grover coin, {walk} coined "
+                            f"steps per bench step, matrix-free lattice kernel",
+                "nx": nx, "ny": nx, "arcs": arcs, "coined_steps_per_bench_step": walk,
+                "psi0": "dense random complex128, np.random.default_rng(rank), normalised",
+                "l2": f"inputs larger than L2: 2 x {16 * arcs / 1e6:.0f} MB ping-pong state (> 126 MB L2)",
+                "parallelism": f"dp{world} (independent lattices per GPU)",
+            },
+            "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
+                         "frac": achieved_gbs / peak, "traffic": traffic,
+                         "kernel": "lattice_step_kernel<flipflop>", "bytes_per_arc": BYTES_PER_ARC,
+                         "peak_source": peak_src, "frac_of_spec_8TBps": achieved_gbs / SPEC_HBM_GBS,
+                         "time_per_launch_us": per_launch_s * 1e6},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 16 * arcs,
+                    "d2h_bytes_per_step": 16 * arcs,
+                    "call": "coined.simulate(engine, spec, (1000, 1001, 1), psi0) -> [WalkState]",
+                    "ms_per_call": e2e_s / len(e2e_times) * 1e3},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "also": extras,
+        }
+        print(json.dumps(line), flush=True)
+    q.stop_engine(eng)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def measure_extras(q, CO, eng, dev, peak):
+    import torch
+    out = {}
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize(dev)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        return a.elapsed_time(b) / 1e3
+
+    # C3 size: 4096^2 torus, one marked vertex (the search oracle), 200 steps
+    nx = 4096
+    g = q.graphs.grid(nx, nx)
+    c = nx // 2 + nx * (nx // 2)
+    spec = q.CoinedSpec(g, "flipflop", "grover", frozenset({c}), "minus_identity")
+    r = CO._LatticeRunner(eng, spec)
+    r.a.fill_(1.0 / np.sqrt(4 * nx * nx))
+    s = timed(lambda: r.advance(200), 3)
+    arcs = 4 * nx * nx
+    per = s / 600
+    gbs = 32 * arcs / per / 1e9
+    out["grid4096_marked"] = {"arc_updates_per_s": arcs / per, "achieved_GBps": gbs, "frac": gbs / peak,
+                              "us_per_step": per * 1e6}
+    del r
+    torch.cuda.empty_cache()
+    # K1: device-built CSR U at 2048^2, SpMV per step (120 B/arc algorithmic)
+    nx = 2048
+    g = q.graphs.grid(nx, nx)
+    spec = q.CoinedSpec(g)
+    t0 = time.perf_counter()
+    u = CO.device_operator(eng, g, "flipflop")
+    torch.cuda.synchronize(dev)
+    build_s = time.perf_counter() - t0
+    n = u.n_rows
+    xa = torch.full((n,), 1.0 / np.sqrt(n), dtype=torch.complex128, device=dev)
+    xb = torch.empty_like(xa)
+
+    def csr_step():
+        q.backend.spmv_device(eng, u, xa, xb)
+    s = timed(csr_step, 50)
+    per = s / 50
+    csr_bytes = 32 + 4 * (16 + 4) + 8
+    gbs = csr_bytes * n / per / 1e9
+    out["csr_spmv_grid2048"] = {"arc_updates_per_s": n / per, "achieved_GBps": gbs, "frac": gbs / peak,
+                                "bytes_per_arc": csr_bytes, "us_per_step": per * 1e6,
+                                "device_build_s": build_s}
+    return out
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

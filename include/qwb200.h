@@ -1,0 +1,197 @@
+/*
+ * qwb200.h — C ABI of the B200 (sm_100a) quantum-walk inner core, libqwb200.so.
+ *
+ * This is the drop-in boundary that replaces the CPU linear-algebra backend of
+ * the reference `qwalk` 0.1.0 (the Neblina-bridge analogue) and
+ * the numpy bodies of its operator builders, step loops and reducers.  Every
+ * entry point names the reference interface it replaces as
+ * `file:line` under /root/reference/pkg/src/qwalk/.
+ *
+ * Conventions
+ *  - Plain C types only: pointers, sizes, doubles.  No torch types.
+ *  - All array arguments are DEVICE pointers owned by the caller, unless the
+ *    name ends in `_host`.  Complex128 is `qwb_z` = {re, im}, 16 bytes,
+ *    layout-identical to numpy/torch complex128.
+ *  - Every call is stream-ordered on `stream` (a cudaStream_t, NULL = legacy
+ *    default stream).  Calls that return a host scalar synchronise `stream`.
+ *  - Return value: QWB_OK (0) or a status code; the message is available from
+ *    qwb_last_error().  Status codes map 1:1 onto the reference's exception
+ *    classes (errors.py:9-104); see QWB_E_* below.
+ *  - Arithmetic contract: results are bitwise equal to the reference's numpy
+ *    arithmetic (products `values * x[cols]` with numpy's FMA complex multiply,
+ *    row sums with numpy's pairwise `add.reduceat` order, |z| with numpy's SIMD
+ *    cabs).  See DESIGN.md §Numerics.
+ *  - A context is used by one host thread at a time (mirrors Engine,
+ *    backend.py:259-267).
+ */
+#ifndef QWB200_H
+#define QWB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.py class each maps to) ------------------------ */
+#define QWB_OK                        0
+#define QWB_E_DIMENSION               1   /* DimensionMismatch            errors.py:27  */
+#define QWB_E_NONFINITE               2   /* NonFiniteEntry               errors.py:36  */
+#define QWB_E_NOT_ON_DEVICE           3   /* NotOnDevice                  errors.py:31  */
+#define QWB_E_ENGINE_STOPPED          4   /* EngineStopped                errors.py:23  */
+#define QWB_E_ALREADY_STOPPED         5   /* AlreadyStopped               errors.py:19  */
+#define QWB_E_UNSUPPORTED             6   /* UnsupportedEngineKind        errors.py:15  */
+#define QWB_E_SERIES_NOT_CONVERGED    7   /* SeriesNotConverged           errors.py:80  */
+#define QWB_E_MARKED_OUT_OF_RANGE     8   /* MarkedVertexOutOfRange       errors.py:76  */
+#define QWB_E_PERSISTENT_SHIFT        9   /* UnsupportedGraphForPersistentShift errors.py:93 */
+#define QWB_E_INVALID_ARGUMENT       10   /* ValueError                                  */
+#define QWB_E_CUDA                   20   /* CUDA runtime failure (QuantumWalkError)      */
+#define QWB_E_NCCL                   21   /* reserved: multi-GPU transport failure        */
+#define QWB_E_OUT_OF_MEMORY          22   /* device allocation failed                     */
+
+/* graph families (graphs.py:115-159) */
+#define QWB_FAMILY_GENERIC    0
+#define QWB_FAMILY_CYCLE      1
+#define QWB_FAMILY_LINE       2
+#define QWB_FAMILY_GRID       3
+#define QWB_FAMILY_HYPERCUBE  4
+
+/* shifts (coined.py:54) */
+#define QWB_SHIFT_FLIPFLOP    0
+#define QWB_SHIFT_PERSISTENT  1
+#define QWB_SHIFT_NONE        2   /* identity: builds the coin C alone (grover_coin) */
+
+typedef struct qwb_ctx qwb_ctx;
+typedef struct { double re, im; } qwb_z;
+
+/* ---- engine lifecycle: init_engine / stop_engine (backend.py:291-314) --- */
+int         qwb_init(int device, qwb_ctx** out);
+int         qwb_shutdown(qwb_ctx* ctx);
+const char* qwb_last_error(const qwb_ctx* ctx);   /* ctx may be NULL: thread-local */
+const char* qwb_version(void);
+int         qwb_device_count(int* count_host);
+
+/* ---- graph builders (graphs.py:115-159, bit-exact int64 CSR) ------------
+ * Two-phase: call with col == NULL to fill row_offsets[n+1] and *nnz_host,
+ * then again with col sized *nnz_host.  params: cycle/line {n},
+ * grid {nx, ny, periodic}, hypercube {dim}.                                  */
+int qwb_family_adjacency(qwb_ctx* ctx, int family, const int64_t* params_host,
+                         int64_t* row_offsets, int64_t* col, int64_t* nnz_host,
+                         void* stream);
+
+/* ---- coined operator builder U = S C with the -I oracle ------------------
+ * replaces coined.evolution_operator / grover_coin / apply_marked_policy /
+ * _shift_targets (coined.py:164-238) and csr_from_triplets (backend.py:195-236).
+ * adj_*: graph adjacency CSR (sorted, int64).  marked: sorted unique vertex ids
+ * (device, may be NULL when n_marked == 0).  shift: QWB_SHIFT_*; family/params
+ * are needed for the persistent shift only.  Two-phase like above:
+ * u_col == NULL -> fill u_row_offsets[n_arcs+1] and *nnz_host.              */
+int qwb_coined_operator(qwb_ctx* ctx, int64_t n, const int64_t* adj_offs,
+                        const int64_t* adj_col, const int64_t* marked, int64_t n_marked,
+                        int shift, int family, const int64_t* params_host,
+                        int64_t* u_row_offsets, int32_t* u_col, qwb_z* u_val,
+                        int64_t* nnz_host, void* stream);
+
+/* src[r] = k with S e_k = e_r for the shift permutation S (flip-flop: the
+ * reverse arc, coined.py:96-101, 222-227; persistent: coined.py:104-146;
+ * NONE: identity).  The permutation CSR of flip_flop_shift / persistent_shift
+ * is then rows r -> single column src[r].                                    */
+int qwb_shift_sources(qwb_ctx* ctx, int64_t n, const int64_t* adj_offs, const int64_t* adj_col,
+                      int shift, int family, const int64_t* params_host, int64_t* src,
+                      void* stream);
+
+/* ---- Hamiltonian H = -gamma A - sum_M |v><v| (ctqw.py:84-98) -------------
+ * h_row_offsets[n+1], h_col/h_val[nnz_adj + n_marked]; marked sorted unique. */
+int qwb_hamiltonian(qwb_ctx* ctx, int64_t n, const int64_t* adj_offs, const int64_t* adj_col,
+                    double gamma, const int64_t* marked, int64_t n_marked,
+                    int64_t* h_row_offsets, int32_t* h_col, qwb_z* h_val, void* stream);
+
+/* ||M||_inf = max_i sum_j |M_ij| with numpy's cabs + pairwise row sums
+ * (ctqw.py:112-120).                                                         */
+int qwb_inf_norm(qwb_ctx* ctx, int64_t n_rows, const int64_t* row_offsets, const qwb_z* val,
+                 double* result_host, void* stream);
+
+/* generic host-assembled CSR upload helper: int64 -> int32 column indices,
+ * with the structural checks of CsrMatrix.validate (backend.py:130-147).     */
+int qwb_csr_prepare(qwb_ctx* ctx, int64_t n_rows, int64_t n_cols, const int64_t* row_offsets,
+                    const int64_t* col64, const qwb_z* val, int64_t nnz, int32_t* col32,
+                    void* stream);
+
+/* ---- CSR SpMV y = M x (backend.matvec_mul / _csr_rows, backend.py:394-430) */
+int qwb_spmv(qwb_ctx* ctx, int64_t n_rows, const int64_t* row_offsets, const int32_t* col,
+             const qwb_z* val, const qwb_z* x, qwb_z* y, void* stream);
+
+/* Repeated SpMV: the coined.simulate loop (coined.py:263-272).  Writes
+ * snapshots U^{k_j} psi0 for the non-decreasing step counts k_host[0..n_snap)
+ * into snaps[j * n_rows ...].  Small operators run the whole loop in one
+ * persistent CTA with the state in shared memory.  scratch: 2*n_rows qwb_z. */
+int qwb_csr_run(qwb_ctx* ctx, int64_t n_rows, const int64_t* row_offsets, const int32_t* col,
+                const qwb_z* val, const qwb_z* psi0, const int64_t* k_host, int64_t n_snap,
+                qwb_z* snaps, qwb_z* scratch, void* stream);
+
+/* ---- matrix-free periodic lattice (nx, ny >= 3), flip-flop or persistent --
+ * Internal state layout: four direction planes [D, L, R, U] of nx*ny qwb_z
+ * each ("planes").  Conversions to/from the reference arc order are exact
+ * permutations.  marked_bits: bitmap over vertices (NULL = none).           */
+/* marked-vertex bitmap bits[(n+31)/32] from a device list (range-checked:
+ * QWB_E_MARKED_OUT_OF_RANGE, coined.py:79-81 / ctqw.py:79-81).               */
+int qwb_marked_bitmap(qwb_ctx* ctx, int64_t n, const int64_t* marked, int64_t n_marked,
+                      uint32_t* bits, void* stream);
+int qwb_lattice_to_planes(qwb_ctx* ctx, int64_t nx, int64_t ny, const qwb_z* arcs, qwb_z* planes,
+                          void* stream);
+int qwb_lattice_from_planes(qwb_ctx* ctx, int64_t nx, int64_t ny, const qwb_z* planes, qwb_z* arcs,
+                            void* stream);
+/* Run `steps` coined steps ping-ponging between a (input) and b.  On return
+ * *final_in_b_host says where the result is.  If trace != NULL, trace[s*n_trace+j]
+ * receives p(trace_vertices_host[j]) of the state BEFORE step s (s < steps),
+ * fused into the step kernel (coined.probability_distribution semantics).  */
+int qwb_lattice_run(qwb_ctx* ctx, int64_t nx, int64_t ny, int shift, const uint32_t* marked_bits,
+                    qwb_z* a, qwb_z* b, int64_t steps, const int64_t* trace_vertices_host,
+                    int n_trace, double* trace, int* final_in_b_host, void* stream);
+/* One step with an optional fused full distribution p of the INPUT state.    */
+int qwb_lattice_step(qwb_ctx* ctx, int64_t nx, int64_t ny, int shift, const uint32_t* marked_bits,
+                     const qwb_z* in, qwb_z* out, double* prob_in, void* stream);
+/* p[v] of a planes state (coined.py:275-294).                                */
+int qwb_lattice_probability(qwb_ctx* ctx, int64_t nx, int64_t ny, const qwb_z* planes, double* p,
+                            void* stream);
+
+/* ---- reducers -------------------------------------------------------------
+ * coined: p[v] = sum over v's arc span of |psi|^2 (coined.py:275-294)
+ * ctqw:   p = |psi|^2                              (ctqw.py:205-212)          */
+int qwb_prob_arcs(qwb_ctx* ctx, int64_t n, const int64_t* tail_offsets, const qwb_z* psi,
+                  double* p, void* stream);
+int qwb_prob_abs2(qwb_ctx* ctx, int64_t n, const qwb_z* psi, double* p, void* stream);
+
+/* ---- BLAS-1 (backend.py:433-464) ------------------------------------------ */
+int qwb_axpy(qwb_ctx* ctx, int64_t n, qwb_z alpha, const qwb_z* x, const qwb_z* y, qwb_z* out,
+             void* stream);                                   /* out = y + alpha x */
+int qwb_scale(qwb_ctx* ctx, int64_t n, qwb_z alpha, const qwb_z* x, qwb_z* out, void* stream);
+int qwb_dot(qwb_ctx* ctx, int64_t n, const qwb_z* x, const qwb_z* y, qwb_z* result_host,
+            void* stream);                                    /* conj(x) . y       */
+int qwb_norm(qwb_ctx* ctx, int64_t n, const qwb_z* x, double* result_host, void* stream);
+/* _check_finite (backend.py:60-62): *all_finite_host = 1 iff no NaN/Inf.     */
+int qwb_check_finite(qwb_ctx* ctx, int64_t n_doubles, const double* x, int* all_finite_host,
+                     void* stream);
+
+/* ---- continuous-time walk: evolve_state (ctqw.py:123-171) ----------------
+ * psi (in/out, device, n entries) <- [T_s(tau H)]^substeps psi, where each
+ * sub-step sums Taylor terms term_k = (-i tau / k) H term_{k-1} until
+ * ||term_k|| <= floor (= tol * ||psi_in||), at most max_terms per sub-step
+ * (else QWB_E_SERIES_NOT_CONVERGED).  The caller computes substeps and tau
+ * exactly as ctqw.py:149-150 does.  terms_host (nullable, [substeps]) gets
+ * the term count of each sub-step.  work: 3*n qwb_z.                         */
+int qwb_taylor_evolve_csr(qwb_ctx* ctx, int64_t n, const int64_t* row_offsets, const int32_t* col,
+                          const qwb_z* val, qwb_z* psi, qwb_z* work, int64_t substeps, double tau,
+                          double floor, int max_terms, int* terms_host, void* stream);
+/* matrix-free H = -gamma A(hypercube dim) - sum_M |v><v| (marked_bits bitmap). */
+int qwb_taylor_evolve_hypercube(qwb_ctx* ctx, int dim, double gamma, const uint32_t* marked_bits,
+                                qwb_z* psi, qwb_z* work, int64_t substeps, double tau, double floor,
+                                int max_terms, int* terms_host, void* stream);
+/* one matrix-free hypercube H x (for tests / backend parity). */
+int qwb_hypercube_apply(qwb_ctx* ctx, int dim, double gamma, const uint32_t* marked_bits,
+                        const qwb_z* x, qwb_z* y, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QWB200_H */

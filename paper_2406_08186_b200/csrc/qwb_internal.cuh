@@ -1,0 +1,65 @@
+// qwb_internal.cuh — context, error plumbing and launch helpers shared by the
+// libqwb200 translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string>
+
+#include "../../include/qwb200.h"
+#include "qwb_numerics.cuh"
+
+struct qwb_ctx {
+  int device;
+  int num_sms;
+  bool stopped;
+  // stream-ordered scratch (grown on demand)
+  void* ws;
+  size_t ws_bytes;
+  // pinned host staging for small readbacks
+  void* pinned;
+  std::string last_error;
+};
+
+namespace qwb {
+
+void set_error(qwb_ctx* ctx, const char* fmt, ...);
+int cuda_status(qwb_ctx* ctx, cudaError_t e, const char* what);
+// scratch of at least `bytes` (256-B aligned), stream-ordered
+int workspace(qwb_ctx* ctx, size_t bytes, cudaStream_t s, void** out);
+int begin(qwb_ctx* ctx);   // checks ctx alive and sets the device
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline unsigned blocks_for(int64_t n, int threads, int64_t cap = 1 << 30) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return static_cast<unsigned>(b);
+}
+
+}  // namespace qwb
+
+#define QWB_BEGIN(ctx)                   \
+  do {                                   \
+    int _st = qwb::begin(ctx);           \
+    if (_st != QWB_OK) return _st;       \
+  } while (0)
+
+#define QWB_CUDA(ctx, call)                                           \
+  do {                                                                \
+    cudaError_t _e = (call);                                          \
+    if (_e != cudaSuccess) return qwb::cuda_status(ctx, _e, #call);   \
+  } while (0)
+
+#define QWB_LAUNCH_CHECK(ctx, what)                                   \
+  do {                                                                \
+    cudaError_t _e = cudaGetLastError();                              \
+    if (_e != cudaSuccess) return qwb::cuda_status(ctx, _e, what);    \
+  } while (0)
+
+#define QWB_FAIL(ctx, code, ...)            \
+  do {                                      \
+    qwb::set_error(ctx, __VA_ARGS__);       \
+    return (code);                          \
+  } while (0)

@@ -1,0 +1,279 @@
+// taylor.cu — continuous-time walk: the sub-stepped truncated Taylor action of
+// exp(-i H t) (ctqw.evolve_state, ctqw.py:123-171).
+//
+// Reference inner loop per term k (ctqw.py:158-165), four engine calls plus four
+// isfinite passes:
+//     hterm = H term;  term = (-1j*tau/k) * hterm;  acc = acc + 1.0*term;
+//     stop when ||term|| <= tol * ||psi_in||
+// Here ONE fused kernel per term reads term_{k-1} (neighbour gathers), writes
+// term_k, read-modify-writes acc and emits per-block ||term_k||^2 partials; a
+// one-block kernel finishes the norm in a fixed order and raises a device
+// `done` flag.  Term kernels launched after `done` return immediately, so the
+// host launches terms speculatively in chunks and synchronises once per chunk
+// instead of once per term.
+//
+// Arithmetic is the reference's bit for bit (numpy complex multiply model,
+// pairwise row sums, Python's complex scalar (0.0, -tau/k)); only the stop
+// test's norm is a different (deterministic) summation order than BLAS dnrm2,
+// which can flip the stop decision only when ||term|| is within a few ulps of
+// the floor.
+//
+// Operators: CSR H (any graph, built by qwb_hamiltonian) and matrix-free
+// hypercube H = -gamma A - sum_M |v><v| whose row v lists, in ascending column
+// order, v with its set bits cleared high->low, the diagonal (if v marked),
+// then v with its clear bits set low->high.
+#include "qwb_internal.cuh"
+
+namespace {
+
+using qwb::cadd;
+using qwb::cmul_np;
+
+constexpr int kTermBlocks = 2048;   // fixed grid => deterministic partial order
+constexpr int kTermThreads = 256;
+
+// Streaming x0 + pairwise(x1..x{L-1}) for rows of L <= 65 entries, element by
+// element in order (numpy block rule with four rotating complex accumulators).
+struct StreamRow {
+  int m, main_end, i;
+  double2 x0, c0, c1, c2, c3, r;
+  __device__ __forceinline__ void init(int L) {
+    m = L - 1;
+    main_end = m >= 4 ? m - (m % 4) : 0;
+    i = -1;
+    r = make_double2(-0.0, -0.0);
+  }
+  __device__ __forceinline__ void push(double2 e) {
+    if (i < 0) {
+      x0 = e;
+      i = 0;
+      return;
+    }
+    if (i < main_end) {
+      c0 = (i < 4) ? e : cadd(c0, e);
+      const double2 t = c0;
+      c0 = c1;
+      c1 = c2;
+      c2 = c3;
+      c3 = t;
+      if (i + 1 == main_end) r = cadd(cadd(c0, c1), cadd(c2, c3));
+    } else {
+      r = cadd(r, e);
+    }
+    ++i;
+  }
+  __device__ __forceinline__ double2 result() const { return m == 0 ? x0 : cadd(x0, r); }
+};
+
+struct CsrOp {
+  const int64_t* __restrict__ offs;
+  const int32_t* __restrict__ col;
+  const double2* __restrict__ val;
+  struct Get {
+    const int32_t* __restrict__ col;
+    const double2* __restrict__ val;
+    const double2* __restrict__ x;
+    int64_t base;
+    __device__ __forceinline__ double2 operator()(int64_t i) const {
+      const int64_t j = base + i;
+      return cmul_np(__ldg(val + j), __ldg(x + __ldg(col + j)));
+    }
+  };
+  __device__ __forceinline__ double2 row(int64_t v, const double2* __restrict__ x) const {
+    const int64_t s = offs[v], e = offs[v + 1];
+    if (e == s) return make_double2(0.0, 0.0);
+    Get g{col, val, x, s};
+    return qwb::reduceat_z(g, e - s);
+  }
+};
+
+template <int MAXD>
+struct HypercubeOp {
+  int dim;
+  double gamma;
+  const uint32_t* __restrict__ bits;
+  __device__ __forceinline__ double2 row(int64_t v, const double2* __restrict__ x) const {
+    double2 xs[MAXD];
+#pragma unroll
+    for (int b = 0; b < MAXD; ++b)
+      if (b < dim) xs[b] = __ldg(x + (v ^ (1LL << b)));
+    const bool mk = bits && ((__ldg(bits + (v >> 5)) >> (v & 31)) & 1u);
+    const double2 g = make_double2(-gamma, 0.0);
+    StreamRow sr;
+    sr.init(dim + (mk ? 1 : 0));
+#pragma unroll
+    for (int b = MAXD - 1; b >= 0; --b)
+      if (b < dim && ((v >> b) & 1)) sr.push(cmul_np(g, xs[b]));
+    if (mk) sr.push(cmul_np(make_double2(-1.0, 0.0), __ldg(x + v)));
+#pragma unroll
+    for (int b = 0; b < MAXD; ++b)
+      if (b < dim && !((v >> b) & 1)) sr.push(cmul_np(g, xs[b]));
+    return sr.result();
+  }
+};
+
+template <class Op>
+__global__ void __launch_bounds__(kTermThreads)
+term_kernel(Op op, int64_t n, const double2* __restrict__ tin, double2* __restrict__ tout,
+            const double2* acc_in, double2* acc_out, double s_k, const int* __restrict__ done,
+            double* __restrict__ partial) {
+  if (*done) return;
+  __shared__ double sh[kTermThreads];
+  const double2 alpha = make_double2(0.0, -s_k);      // Python complex(-1j * tau / k)
+  const double2 one = make_double2(1.0, 0.0);
+  double nrm = 0.0;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const double2 h = op.row(v, tin);
+    const double2 t = cmul_np(alpha, h);
+    tout[v] = t;
+    acc_out[v] = cadd(acc_in[v], cmul_np(one, t));
+    nrm = __fma_rn(t.x, t.x, __fma_rn(t.y, t.y, nrm));
+  }
+  sh[threadIdx.x] = nrm;
+  __syncthreads();
+  for (int s = kTermThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__global__ void __launch_bounds__(kTermThreads)
+term_finalize_kernel(const double* __restrict__ partial, int nparts, double floor_, int k,
+                     int* __restrict__ done, int* __restrict__ terms) {
+  if (*done) return;
+  __shared__ double sh[kTermThreads];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) acc = __dadd_rn(acc, partial[i]);
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = kTermThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (__dsqrt_rn(sh[0]) <= floor_) {
+      *done = 1;
+      *terms = k;
+    }
+  }
+}
+
+__global__ void apply_kernel_hc(HypercubeOp<32> op, int64_t n, const double2* __restrict__ x,
+                                double2* __restrict__ y) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    y[v] = op.row(v, x);
+}
+
+template <class Op>
+int evolve(qwb_ctx* ctx, const Op& op, int64_t n, double2* psi, double2* work, int64_t substeps,
+           double tau, double floor_, int max_terms, int* terms_host, cudaStream_t s) {
+  if (substeps < 1) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "substeps must be >= 1");
+  if (max_terms < 1) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "max_terms must be >= 1");
+  void* ws;
+  int st = qwb::workspace(ctx, kTermBlocks * sizeof(double) + 256, s, &ws);
+  if (st) return st;
+  double* partial = reinterpret_cast<double*>(ws);
+  int* flags = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + kTermBlocks * sizeof(double));
+  int* pin = reinterpret_cast<int*>(ctx->pinned);
+  // 4 distinct buffers: cur, acc, term ping-pong
+  double2* bufs[4] = {psi, work, work + n, work + 2 * n};
+  int cur = 0;
+  int prev_terms = 8;
+  for (int64_t sub = 0; sub < substeps; ++sub) {
+    int others[3], j = 0;
+    for (int b = 0; b < 4; ++b)
+      if (b != cur) others[j++] = b;
+    double2* acc = bufs[others[0]];
+    double2* ta = bufs[others[1]];
+    double2* tb = bufs[others[2]];
+    QWB_CUDA(ctx, cudaMemsetAsync(flags, 0, 2 * sizeof(int), s));
+    int launched = 0;
+    int chunk = prev_terms + 1;
+    bool done = false;
+    while (!done) {
+      if (launched >= max_terms) {
+        QWB_FAIL(ctx, QWB_E_SERIES_NOT_CONVERGED,
+                 "series did not reach the tolerance within %d terms per sub-step", max_terms);
+      }
+      const int upto = launched + chunk < max_terms ? launched + chunk : max_terms;
+      for (int k = launched + 1; k <= upto; ++k) {
+        const double2* tin = (k == 1) ? bufs[cur] : ((k % 2) ? tb : ta);
+        double2* tout = (k % 2) ? ta : tb;
+        const double2* ain = (k == 1) ? bufs[cur] : acc;
+        const double s_k = tau / (double)k;
+        term_kernel<Op><<<kTermBlocks, kTermThreads, 0, s>>>(op, n, tin, tout, ain, acc, s_k, flags,
+                                                             partial);
+        term_finalize_kernel<<<1, kTermThreads, 0, s>>>(partial, kTermBlocks, floor_, k, flags,
+                                                        flags + 1);
+      }
+      QWB_LAUNCH_CHECK(ctx, "term kernels");
+      launched = upto;
+      QWB_CUDA(ctx, cudaMemcpyAsync(pin, flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+      QWB_CUDA(ctx, cudaStreamSynchronize(s));
+      done = pin[0] != 0;
+      chunk = 4;
+    }
+    prev_terms = pin[1];
+    if (terms_host) terms_host[sub] = pin[1];
+    cur = others[0];   // acc becomes the current state
+  }
+  if (bufs[cur] != psi)
+    QWB_CUDA(ctx, cudaMemcpyAsync(psi, bufs[cur], n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+  return QWB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int qwb_taylor_evolve_csr(qwb_ctx* ctx, int64_t n, const int64_t* row_offsets, const int32_t* col,
+                          const qwb_z* val, qwb_z* psi, qwb_z* work, int64_t substeps, double tau,
+                          double floor, int max_terms, int* terms_host, void* stream) {
+  QWB_BEGIN(ctx);
+  if (n < 1) QWB_FAIL(ctx, QWB_E_DIMENSION, "dimension must be positive");
+  CsrOp op{row_offsets, col, reinterpret_cast<const double2*>(val)};
+  return evolve(ctx, op, n, reinterpret_cast<double2*>(psi), reinterpret_cast<double2*>(work),
+                substeps, tau, floor, max_terms, terms_host, qwb::as_stream(stream));
+}
+
+int qwb_taylor_evolve_hypercube(qwb_ctx* ctx, int dim, double gamma, const uint32_t* marked_bits,
+                                qwb_z* psi, qwb_z* work, int64_t substeps, double tau, double floor,
+                                int max_terms, int* terms_host, void* stream) {
+  QWB_BEGIN(ctx);
+  if (dim < 1 || dim > 32) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "hypercube dim must be in 1..32");
+  const int64_t n = 1LL << dim;
+  double2* p = reinterpret_cast<double2*>(psi);
+  double2* w = reinterpret_cast<double2*>(work);
+  cudaStream_t s = qwb::as_stream(stream);
+  if (dim <= 8) {
+    HypercubeOp<8> op{dim, gamma, marked_bits};
+    return evolve(ctx, op, n, p, w, substeps, tau, floor, max_terms, terms_host, s);
+  }
+  if (dim <= 16) {
+    HypercubeOp<16> op{dim, gamma, marked_bits};
+    return evolve(ctx, op, n, p, w, substeps, tau, floor, max_terms, terms_host, s);
+  }
+  if (dim <= 24) {
+    HypercubeOp<24> op{dim, gamma, marked_bits};
+    return evolve(ctx, op, n, p, w, substeps, tau, floor, max_terms, terms_host, s);
+  }
+  HypercubeOp<32> op{dim, gamma, marked_bits};
+  return evolve(ctx, op, n, p, w, substeps, tau, floor, max_terms, terms_host, s);
+}
+
+int qwb_hypercube_apply(qwb_ctx* ctx, int dim, double gamma, const uint32_t* marked_bits,
+                        const qwb_z* x, qwb_z* y, void* stream) {
+  QWB_BEGIN(ctx);
+  if (dim < 1 || dim > 32) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "hypercube dim must be in 1..32");
+  const int64_t n = 1LL << dim;
+  HypercubeOp<32> op{dim, gamma, marked_bits};
+  apply_kernel_hc<<<qwb::blocks_for(n, 256, (int64_t)ctx->num_sms * 16), 256, 0, qwb::as_stream(stream)>>>(
+      op, n, reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y));
+  QWB_LAUNCH_CHECK(ctx, "apply_kernel_hc");
+  return QWB_OK;
+}
+
+}  // extern "C"
