@@ -216,7 +216,7 @@ def run_reference(args):
     mv.close()
     value = u.n_rows * sample * args.steps / el
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
@@ -249,19 +249,30 @@ def run_b200(args):
     eng = q.init_engine("b200", device=local)
 
     nx = args.nx
-    g = q.graphs.grid(nx, nx)
-    spec = q.CoinedSpec(g)
-    arcs = g.num_arcs
     walk = args.walk_steps
-    rng = np.random.default_rng(0 + rank)
-    psi = rng.normal(size=arcs) + 1j * rng.normal(size=arcs)
-    psi /= np.linalg.norm(psi)
-    basis = q.graphs.arc_basis(g)
-    psi0 = q.WalkState(basis, psi)
+    if world == 1:
+        g = q.graphs.grid(nx, nx)
+        spec = q.CoinedSpec(g)
+        arcs = g.num_arcs
+        rng = np.random.default_rng(0)
+        psi = rng.normal(size=arcs) + 1j * rng.normal(size=arcs)
+        psi /= np.linalg.norm(psi)
+        psi0 = q.WalkState(q.graphs.arc_basis(g), psi)
+        runner = CO._LatticeRunner(eng, spec)
+        x = q.backend.to_device(eng, psi0.amplitudes)
+    else:
+        # weak scaling: one nx x (nx * world) torus, rank r owns rows [r*nx, (r+1)*nx)
+        from paper_2406_08186_b200 import distributed as DI
+        runner = DI.SlabLattice(eng, nx, nx * world, "flipflop", (), rank, world)
+        arcs = 4 * nx * runner.rows
+        rng = np.random.default_rng(rank)
+        psi = rng.normal(size=arcs) + 1j * rng.normal(size=arcs)
+        psi /= np.linalg.norm(psi) * np.sqrt(world)
+        host_local, _owner = q.state._pinned_empty(arcs) or (psi.copy(), None)
+        host_local[...] = psi
+        x = q.backend.to_device(eng, host_local)
 
     # ---- device-resident timed region: runner.advance(walk) per bench step
-    runner = CO._LatticeRunner(eng, spec)
-    x = torch.from_numpy(psi0.amplitudes).to(dev)
     runner.load(x)
     stream = torch.cuda.current_stream(dev)
     for _ in range(args.warmup):
@@ -284,8 +295,10 @@ def run_b200(args):
     clk = clocks.stop()
     el_ms = e0.elapsed_time(e1)
     el_ms = max_over_ranks(el_ms, dist, dev)
-    launches = args.steps * walk
-    per_launch_s = el_ms / 1e3 / launches
+    # one lattice_step_kernel launch per coined step on one GPU; on N > 1 the
+    # step is two launches (boundary rows, interior rows) + the NCCL exchange
+    launches = args.steps * walk * (1 if world == 1 else 2)
+    per_launch_s = el_ms / 1e3 / (args.steps * walk)   # per coined step (all rows)
     value = world * arcs * walk * args.steps / (el_ms / 1e3)
 
     peak, peak_src = peaks()
@@ -295,20 +308,27 @@ def run_b200(args):
 
     # ---- e2e: public API with host buffers, H2D + D2H inside the timed region
     e2e_times = []
-    out_state = None
     for i in range(1 + args.steps):
         if dist:
             dist.barrier()
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        out_state = CO.simulate(eng, spec, (walk, walk + 1, 1), psi0)[0]
+        if world == 1:
+            out = CO.simulate(eng, spec, (walk, walk + 1, 1), psi0)[0].amplitudes
+        else:
+            xd = q.backend.to_device(eng, host_local)
+            runner.load(xd)
+            runner.advance(walk)
+            runner.store(xd)
+            out, _o = q.backend.to_host(xd, pinned=True)
         torch.cuda.synchronize(dev)
         t1 = time.perf_counter()
         if i > 0:
             e2e_times.append(t1 - t0)
     e2e_s = max_over_ranks(sum(e2e_times), dist, dev)
     e2e_value = world * arcs * walk * len(e2e_times) / e2e_s
-    assert abs(out_state.norm() - 1.0) < 1e-9
+    if world == 1:
+        assert abs(np.linalg.norm(out) - 1.0) < 1e-9
 
     extras = {}
     if not args.no_extras and rank == 0:
@@ -328,13 +348,16 @@ def run_b200(args):
             "warmup": args.warmup, "ms_per_step": el_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {
-                "workload": f"C2: grid {nx}x{nx} torus ({nx * nx} vertices, {arcs} arcs; BASELINE configs[1] "
-                            f"'4M vertices, 16M arcs' per SURVEY D1), flip-flop Grover coin, {walk} coined "
-                            f"steps per bench step, matrix-free lattice kernel",
-                "nx": nx, "ny": nx, "arcs": arcs, "coined_steps_per_bench_step": walk,
-                "psi0": "dense random complex128, np.random.default_rng(rank), normalised",
-                "l2": f"inputs larger than L2: 2 x {16 * arcs / 1e6:.0f} MB ping-pong state (> 126 MB L2)",
-                "parallelism": f"dp{world} (independent lattices per GPU)",
+                "workload": (f"C2: grid {nx}x{nx} torus ({nx * nx} vertices, {arcs} arcs; BASELINE configs[1] "
+                             f"'4M vertices, 16M arcs' per SURVEY D1), flip-flop Grover coin, {walk} coined "
+                             f"steps per bench step, matrix-free lattice kernel") if world == 1 else
+                            (f"grid {nx}x{nx * world} torus split in {world} y-slabs of {nx}x{nx} "
+                             f"({arcs} arcs per GPU), flip-flop Grover, {walk} coined steps per bench step, "
+                             f"NCCL halo exchange of 2 rows per step overlapped with interior rows"),
+                "nx": nx, "ny": nx * world, "arcs": arcs * world, "coined_steps_per_bench_step": walk,
+                "psi0": "dense random complex128 (seeded per rank), normalised",
+                "l2": f"inputs larger than L2: 2 x {16 * arcs / 1e6:.0f} MB ping-pong state per GPU (> 126 MB L2)",
+                "parallelism": "dp1" if world == 1 else f"y-slab sharding over {world} GPUs (weak scaling)",
             },
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                          "frac": achieved_gbs / peak, "traffic": traffic,
@@ -344,7 +367,8 @@ def run_b200(args):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 16 * arcs,
                     "d2h_bytes_per_step": 16 * arcs,
-                    "call": "coined.simulate(engine, spec, (1000, 1001, 1), psi0) -> [WalkState]",
+                    "call": "coined.simulate(engine, spec, (1000, 1001, 1), psi0) -> [WalkState]" if world == 1
+                    else "distributed.SlabLattice load(H2D pinned) + advance(1000) + store + D2H per rank",
                     "ms_per_call": e2e_s / len(e2e_times) * 1e3},
             "gpu_launches": launches,
             "clocks": clk,

@@ -155,6 +155,37 @@ int qwb_lattice_step(qwb_ctx* ctx, int64_t nx, int64_t ny, int shift, const uint
 int qwb_lattice_probability(qwb_ctx* ctx, int64_t nx, int64_t ny, const qwb_z* planes, double* p,
                             void* stream);
 
+/* ---- multi-GPU: y-slabs of one periodic lattice, NCCL halo exchange -------
+ * (no reference counterpart: its only parallelism is the in-process row-block
+ * pool, backend.py:426-430; multi-GPU is future work in PAPER.md:499-501).
+ * A rank owns global rows [y0, y0+ny_local) (ny_local >= 2) of an nx x ny
+ * torus; its planes buffers hold 4 x nx x (ny_local + 2) qwb_z (one extra row
+ * each side).  Arc arrays passed to the slab conversions hold only the owned
+ * rows' arcs, i.e. the contiguous range [4*nx*y0, 4*nx*(y0+ny_local)) of the
+ * reference arc order.  Results are bitwise equal to the single-GPU run.     */
+int qwb_slab_to_planes(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local,
+                       const qwb_z* arcs, qwb_z* planes, void* stream);
+int qwb_slab_from_planes(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local,
+                         const qwb_z* planes, qwb_z* arcs, void* stream);
+int qwb_slab_probability(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local,
+                         const qwb_z* planes, double* p, void* stream);
+/* one step without exchange; part 0 = all owned rows, 1 = first+last, 2 = interior */
+int qwb_slab_step(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int shift,
+                  const uint32_t* marked_bits, const qwb_z* in, qwb_z* out, int part, void* stream);
+/* single-device emulation of the per-step exchange between nslabs slabs (tests) */
+int qwb_slab_exchange_local(qwb_ctx* ctx, int64_t nx, int shift, const int64_t* ny_local_host,
+                            qwb_z* const* planes_host, int nslabs, void* stream);
+/* NCCL communicator (one per rank; id: 128 bytes from rank 0, broadcast by the caller) */
+int qwb_comm_unique_id(void* id_out_host);
+int qwb_comm_init(qwb_ctx* ctx, const void* id_host, int nranks, int rank);
+int qwb_comm_destroy(qwb_ctx* ctx);
+/* `steps` steps with the boundary rows computed first, their exchange on a
+ * comm stream overlapped with the interior rows.  marked_bits is a GLOBAL
+ * vertex bitmap (NULL = none).                                                */
+int qwb_slab_run(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int shift,
+                 const uint32_t* marked_bits, qwb_z* a, qwb_z* b, int64_t steps, int rank_below,
+                 int rank_above, int* final_in_b_host, void* stream);
+
 /* ---- reducers -------------------------------------------------------------
  * coined: p[v] = sum over v's arc span of |psi|^2 (coined.py:275-294)
  * ctqw:   p = |psi|^2                              (ctqw.py:205-212)          */

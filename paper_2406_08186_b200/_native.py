@@ -71,6 +71,15 @@ SIGNATURES = {
     "qwb_lattice_run": [_vp, _i64, _i64, _i32, _vp, _vp, _vp, _i64, _p_i64, _i32, _vp, _p_int, _vp],
     "qwb_lattice_step": [_vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _vp],
     "qwb_lattice_probability": [_vp, _i64, _i64, _vp, _vp, _vp],
+    "qwb_slab_to_planes": [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp],
+    "qwb_slab_from_planes": [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp],
+    "qwb_slab_probability": [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp],
+    "qwb_slab_step": [_vp, _i64, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _i32, _vp],
+    "qwb_slab_exchange_local": [_vp, _i64, _i32, _p_i64, C.POINTER(_vp), _i32, _vp],
+    "qwb_comm_unique_id": [_vp],
+    "qwb_comm_init": [_vp, _vp, _i32, _i32],
+    "qwb_comm_destroy": [_vp],
+    "qwb_slab_run": [_vp, _i64, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _i64, _i32, _i32, _p_int, _vp],
     "qwb_prob_arcs": [_vp, _i64, _vp, _vp, _vp, _vp],
     "qwb_prob_abs2": [_vp, _i64, _vp, _vp, _vp],
     "qwb_axpy": [_vp, _i64, qwb_z, _vp, _vp, _vp, _vp],

@@ -1,0 +1,225 @@
+// comm.cu — multi-GPU slab stepping with an NCCL halo exchange.
+//
+// The reference has no distribution beyond an in-process row-block thread
+// pool (backend.py:426-430); PAPER.md:499-501 lists multi-GPU as future work.
+// Here a periodic nx x ny lattice is split into contiguous y-slabs, one per
+// rank/GPU (lattice.cu "Slabs").  Per coined step:
+//
+//   compute stream:  [wait recv(t-1)] boundary rows (first, last) -> record ready
+//   comm stream:     [wait ready] ncclGroupStart; send/recv 2 rows of nx
+//                     complex128 to/from each y-neighbour; ncclGroupEnd -> record done
+//   compute stream:  interior rows (overlaps the exchange)
+//
+// The exchanged rows are the step's outputs that belong to the neighbour
+// (plane U of its last row, plane D of its first row); NCCL receives straight
+// into this rank's planes and sends straight from its two extra rows, so there
+// is no packing.  Volume: 2 x 16 x nx bytes per direction per step.
+//
+// NCCL is dlopen'ed (libnccl.so.2, or $QWB_NCCL_LIB) so the library has no
+// link-time NCCL dependency and shares the NCCL that torch.distributed loaded.
+#include <dlfcn.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "qwb_lattice.cuh"
+
+namespace {
+
+typedef struct {
+  char internal[128];
+} NcclUid;
+typedef void* NcclComm;
+typedef int (*fn_get_uid)(NcclUid*);
+typedef int (*fn_init_rank)(NcclComm*, int, NcclUid, int);
+typedef int (*fn_destroy)(NcclComm);
+typedef int (*fn_sendrecv)(void*, size_t, int, int, NcclComm, cudaStream_t);
+typedef int (*fn_group)(void);
+typedef const char* (*fn_errstr)(int);
+
+constexpr int kNcclFloat64 = 8;
+
+struct Nccl {
+  void* h = nullptr;
+  fn_get_uid get_uid = nullptr;
+  fn_init_rank init_rank = nullptr;
+  fn_destroy destroy = nullptr;
+  fn_sendrecv send = nullptr;
+  fn_sendrecv recv = nullptr;
+  fn_group group_start = nullptr;
+  fn_group group_end = nullptr;
+  fn_errstr errstr = nullptr;
+};
+
+Nccl g_nccl;
+
+int load_nccl(qwb_ctx* ctx) {
+  if (g_nccl.h) return QWB_OK;
+  const char* path = getenv("QWB_NCCL_LIB");
+  void* h = dlopen(path && *path ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) QWB_FAIL(ctx, QWB_E_NCCL, "cannot load NCCL (%s): %s", path ? path : "libnccl.so.2", dlerror());
+  Nccl n;
+  n.h = h;
+  n.get_uid = (fn_get_uid)dlsym(h, "ncclGetUniqueId");
+  n.init_rank = (fn_init_rank)dlsym(h, "ncclCommInitRank");
+  n.destroy = (fn_destroy)dlsym(h, "ncclCommDestroy");
+  // ncclSend's buffer is const; the ABI is identical for our purposes
+  n.send = (fn_sendrecv)dlsym(h, "ncclSend");
+  n.recv = (fn_sendrecv)dlsym(h, "ncclRecv");
+  n.group_start = (fn_group)dlsym(h, "ncclGroupStart");
+  n.group_end = (fn_group)dlsym(h, "ncclGroupEnd");
+  n.errstr = (fn_errstr)dlsym(h, "ncclGetErrorString");
+  if (!n.get_uid || !n.init_rank || !n.destroy || !n.send || !n.recv || !n.group_start ||
+      !n.group_end || !n.errstr)
+    QWB_FAIL(ctx, QWB_E_NCCL, "NCCL library lacks a required symbol");
+  g_nccl = n;
+  return QWB_OK;
+}
+
+#define QWB_NCCL(ctx, call)                                                             \
+  do {                                                                                  \
+    int _r = (call);                                                                    \
+    if (_r != 0) QWB_FAIL(ctx, QWB_E_NCCL, "NCCL error %d (%s) in %s", _r,              \
+                          g_nccl.errstr ? g_nccl.errstr(_r) : "?", #call);              \
+  } while (0)
+
+}  // namespace
+
+extern "C" {
+
+int qwb_comm_unique_id(void* id_out_host) {
+  int st = load_nccl(nullptr);
+  if (st) return st;
+  NcclUid uid;
+  int r = g_nccl.get_uid(&uid);
+  if (r != 0) {
+    qwb::set_error(nullptr, "ncclGetUniqueId failed: %d", r);
+    return QWB_E_NCCL;
+  }
+  memcpy(id_out_host, &uid, sizeof(uid));
+  return QWB_OK;
+}
+
+int qwb_comm_init(qwb_ctx* ctx, const void* id_host, int nranks, int rank) {
+  QWB_BEGIN(ctx);
+  if (ctx->comm) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "communicator already initialised");
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "bad rank %d of %d", rank, nranks);
+  int st = load_nccl(ctx);
+  if (st) return st;
+  NcclUid uid;
+  memcpy(&uid, id_host, sizeof(uid));
+  NcclComm comm = nullptr;
+  QWB_NCCL(ctx, g_nccl.init_rank(&comm, nranks, uid, rank));
+  ctx->comm = comm;
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  QWB_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+  QWB_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming));
+  QWB_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_done, cudaEventDisableTiming));
+  return QWB_OK;
+}
+
+int qwb_comm_destroy(qwb_ctx* ctx) {
+  if (!ctx || !ctx->comm) return QWB_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->comm_stream) cudaStreamSynchronize(ctx->comm_stream);
+  g_nccl.destroy((NcclComm)ctx->comm);
+  ctx->comm = nullptr;
+  if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+  if (ctx->ev_ready) cudaEventDestroy(ctx->ev_ready);
+  if (ctx->ev_done) cudaEventDestroy(ctx->ev_done);
+  ctx->comm_stream = nullptr;
+  ctx->ev_ready = ctx->ev_done = nullptr;
+  ctx->nranks = 1;
+  ctx->rank = 0;
+  return QWB_OK;
+}
+
+// Run `steps` coined steps on this rank's slab, exchanging the two boundary
+// rows with rank_below / rank_above each step.  Result in a (even steps) or
+// b (odd), reported through *final_in_b_host.
+int qwb_slab_run(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int shift,
+                 const uint32_t* marked_bits, qwb_z* a, qwb_z* b, int64_t steps, int rank_below,
+                 int rank_above, int* final_in_b_host, void* stream) {
+  QWB_BEGIN(ctx);
+  qwb::Geom g;
+  int st = qwb::lattice_slab_geom(ctx, nx, ny, y0, ny_local, &g);
+  if (!st) st = qwb::lattice_check_shift(ctx, shift);
+  if (st) return st;
+  if (!ctx->comm) QWB_FAIL(ctx, QWB_E_NCCL, "qwb_comm_init has not been called");
+  if (rank_below < 0 || rank_below >= ctx->nranks || rank_above < 0 || rank_above >= ctx->nranks)
+    QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "neighbour ranks out of range");
+  if (steps < 0) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "steps must be >= 0");
+  cudaStream_t s = qwb::as_stream(stream);
+  cudaStream_t cs = ctx->comm_stream;
+  NcclComm comm = (NcclComm)ctx->comm;
+  const int64_t P = g.pstride;
+  const size_t cnt = 2 * (size_t)nx;   // one row of complex128 as float64s
+  // plane pushed across the lower / upper slab edge: flip-flop writes the
+  // reverse arc (plane U below, plane D above), persistent keeps the direction
+  const int64_t pd = shift == QWB_SHIFT_FLIPFLOP ? 3 : 0, pu = 3 - pd;
+  const qwb::Rows edge = qwb::slab_rows(ny_local, 1);
+  const qwb::Rows inner = qwb::slab_rows(ny_local, 2);
+  qwb::TraceArgs tr{};
+  double2* cur = reinterpret_cast<double2*>(a);
+  double2* nxt = reinterpret_cast<double2*>(b);
+  // the comm stream starts after everything already queued on s
+  QWB_CUDA(ctx, cudaEventRecord(ctx->ev_done, s));
+  for (int64_t k = 0; k < steps; ++k) {
+    QWB_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_done, 0));
+    qwb::lattice_launch(shift, s, g, edge, cur, nxt, marked_bits, nullptr, 0, tr);
+    QWB_CUDA(ctx, cudaEventRecord(ctx->ev_ready, s));
+    QWB_CUDA(ctx, cudaStreamWaitEvent(cs, ctx->ev_ready, 0));
+    double2* send_down = nxt + pd * P;                                 // extra row 0
+    double2* recv_from_up = nxt + pd * P + (int64_t)ny_local * nx;     // last owned row
+    double2* send_up = nxt + pu * P + (int64_t)(ny_local + 1) * nx;    // extra row ny_local+1
+    double2* recv_from_down = nxt + pu * P + (int64_t)nx;              // first owned row
+    QWB_NCCL(ctx, g_nccl.group_start());
+    QWB_NCCL(ctx, g_nccl.send(send_down, cnt, kNcclFloat64, rank_below, comm, cs));
+    QWB_NCCL(ctx, g_nccl.recv(recv_from_up, cnt, kNcclFloat64, rank_above, comm, cs));
+    QWB_NCCL(ctx, g_nccl.send(send_up, cnt, kNcclFloat64, rank_above, comm, cs));
+    QWB_NCCL(ctx, g_nccl.recv(recv_from_down, cnt, kNcclFloat64, rank_below, comm, cs));
+    QWB_NCCL(ctx, g_nccl.group_end());
+    QWB_CUDA(ctx, cudaEventRecord(ctx->ev_done, cs));
+    qwb::lattice_launch(shift, s, g, inner, cur, nxt, marked_bits, nullptr, 0, tr);
+    double2* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+  QWB_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_done, 0));
+  QWB_LAUNCH_CHECK(ctx, "lattice_step_kernel(slab run)");
+  if (final_in_b_host) *final_in_b_host = (steps % 2) ? 1 : 0;
+  return QWB_OK;
+}
+
+// Single-process emulation of the exchange for P slabs held on ONE device
+// (tests): after qwb_slab_step(part=0) on every slab, move the two boundary
+// rows of slab i into its neighbours exactly as qwb_slab_run's NCCL group
+// does.  planes[i] are device pointers to the slabs' output buffers.
+int qwb_slab_exchange_local(qwb_ctx* ctx, int64_t nx, int shift, const int64_t* ny_local_host,
+                            qwb_z* const* planes_host, int nslabs, void* stream) {
+  QWB_BEGIN(ctx);
+  int st = qwb::lattice_check_shift(ctx, shift);
+  if (st) return st;
+  cudaStream_t s = qwb::as_stream(stream);
+  const size_t bytes = 16 * (size_t)nx;
+  const int64_t pd = shift == QWB_SHIFT_FLIPFLOP ? 3 : 0, pu = 3 - pd;
+  for (int i = 0; i < nslabs; ++i) {
+    const int below = (i + nslabs - 1) % nslabs, above = (i + 1) % nslabs;
+    const int64_t nl = ny_local_host[i];
+    const int64_t P = nx * (nl + 2);
+    double2* me = reinterpret_cast<double2*>(planes_host[i]);
+    // my extra row 0 -> below's last owned row (plane pd)
+    const int64_t nlb = ny_local_host[below], Pb = nx * (nlb + 2);
+    double2* bl = reinterpret_cast<double2*>(planes_host[below]);
+    QWB_CUDA(ctx, cudaMemcpyAsync(bl + pd * Pb + nlb * nx, me + pd * P, bytes, cudaMemcpyDeviceToDevice, s));
+    // my extra row ny_local+1 -> above's first owned row (plane pu)
+    const int64_t nla = ny_local_host[above], Pa = nx * (nla + 2);
+    double2* ab = reinterpret_cast<double2*>(planes_host[above]);
+    QWB_CUDA(ctx, cudaMemcpyAsync(ab + pu * Pa + nx, me + pu * P + (nl + 1) * nx, bytes,
+                                  cudaMemcpyDeviceToDevice, s));
+  }
+  return QWB_OK;
+}
+
+}  // extern "C"

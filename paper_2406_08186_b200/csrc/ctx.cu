@@ -100,6 +100,12 @@ int qwb_init(int device, qwb_ctx** out) {
   c->ws = nullptr;
   c->ws_bytes = 0;
   c->pinned = nullptr;
+  c->comm = nullptr;
+  c->nranks = 1;
+  c->rank = 0;
+  c->comm_stream = nullptr;
+  c->ev_ready = nullptr;
+  c->ev_done = nullptr;
   e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaMallocHost(&c->pinned, 4096);
   if (e != cudaSuccess) {
@@ -121,6 +127,7 @@ int qwb_shutdown(qwb_ctx* ctx) {
   }
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
+  if (ctx->comm) qwb_comm_destroy(ctx);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   ctx->ws = nullptr;

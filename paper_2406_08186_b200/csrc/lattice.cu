@@ -5,11 +5,11 @@
 // with U = S C built by coined.evolution_operator (coined.py:230-238).
 //
 // State layout in HBM ("planes"): four direction planes [D, L, R, U], each a
-// dense nx*ny complex128 array indexed by vertex id v = x + nx*y, holding the
-// amplitude of the arc leaving v towards its down/left/right/up neighbour.  The
-// reference's arc order (tail-major, heads ascending, graphs.py:178-194) is a
-// per-vertex permutation of the same four values whose slot order depends on
-// the vertex position class:
+// dense (rows x nx) complex128 array indexed by vertex (x, y), holding the
+// amplitude of the arc leaving the vertex towards its down/left/right/up
+// neighbour.  The reference's arc order (tail-major, heads ascending,
+// graphs.py:178-194) is a per-vertex permutation of the same four values whose
+// slot order depends on the vertex position class:
 //     interior          D L R U
 //     x in {0, nx-1}    D R L U
 //     y == 0            L R U D   (R L U D on x edges)
@@ -19,28 +19,35 @@
 // Step (push form).  Vertex w reads its 4 amplitudes (4 coalesced 16-B loads),
 // forms for every direction e the row value
 //     O_e(w) = p0 + ((p1 + p2) + p3),  p_i = (i == slot(e) ? -0.5 : 0.5) * s_i
-// with s_i the amplitudes in w's reference slot order (this is exactly
-// numpy's reduceat over U's row), or O_e(w) = -psi_e(w) when w
-// is marked (the -I oracle, coined.py:188-219), and stores it to
+// with s_i the amplitudes in w's reference slot order (exactly numpy's
+// reduceat over U's row), or O_e(w) = -psi_e(w) when w is
+// marked (the -I oracle, coined.py:188-219), and stores it to
 //     flip-flop : plane(-e)[w + e]     (row (w+e, w) of U)
 //     persistent: plane(e)[w + e]      (row (w+e, w+2e) of U)
-// i.e. 4 shifted-but-coalesced 16-B stores.  No shared memory and no halo:
-// every byte of psi is read once and every byte of psi' written once, 32 B per
-// arc per step — the HBM roofline of this operator.
-#include "qwb_internal.cuh"
+// i.e. 4 shifted-but-coalesced 16-B stores.  No shared memory and no halo
+// reads: every byte of psi is read once and every byte of psi' written once,
+// 32 B per arc per step — the HBM roofline of this operator.
+//
+// Slabs (multi-GPU).  A rank owns global rows [y0, y0 + ny_local) of an
+// nx x ny torus, stored as local rows 1..ny_local of planes with one extra row
+// on each side (local rows 0 and ny_local + 1).  Because the step is a push,
+// a slab needs NO halo input: the only outputs it cannot produce are plane D
+// of its first row and plane U of its last row, which the neighbours push into
+// their own extra rows.  Exchanging those two nx-long rows per step (NCCL
+// send/recv, comm.cu) completes the state.  Position classes use GLOBAL y, so
+// every arc is computed by the same formula as on one GPU: sharded results are
+// bitwise identical to the single-GPU run.
+#include "qwb_lattice.cuh"
 
 namespace {
 
 using qwb::abs2_np;
 using qwb::cadd;
 using qwb::cmul_np;
-
-constexpr int kMaxTrace = 8;
-struct TraceArgs {
-  int n;
-  int64_t v[kMaxTrace];
-  double* out;
-};
+using qwb::Geom;
+using qwb::kMaxTrace;
+using qwb::Rows;
+using qwb::TraceArgs;
 
 // numpy product (c + 0i) * a
 __device__ __forceinline__ double2 scale_np(double c, double2 a) {
@@ -48,22 +55,21 @@ __device__ __forceinline__ double2 scale_np(double c, double2 a) {
 }
 
 struct Slots {
-  // amplitudes in reference slot order and the slot of each direction
-  double2 s0, s1, s2, s3;
-  int pD, pL, pR, pU;
+  double2 s0, s1, s2, s3;   // amplitudes in reference slot order
+  int pD, pL, pR, pU;       // slot of each direction
 };
 
-__device__ __forceinline__ Slots order_slots(int x, int y, int nx, int ny, double2 vD, double2 vL,
+__device__ __forceinline__ Slots order_slots(int x, int gy, int nx, int ny, double2 vD, double2 vL,
                                              double2 vR, double2 vU) {
   Slots o;
   const bool xe = (x == 0) | (x == nx - 1);
   const double2 h0 = xe ? vR : vL;
   const double2 h1 = xe ? vL : vR;
   int ph0, ph1;
-  if (y == 0) {
+  if (gy == 0) {
     o.s0 = h0; o.s1 = h1; o.s2 = vU; o.s3 = vD;
     ph0 = 0; ph1 = 1; o.pU = 2; o.pD = 3;
-  } else if (y == ny - 1) {
+  } else if (gy == ny - 1) {
     o.s0 = vU; o.s1 = vD; o.s2 = h0; o.s3 = h1;
     o.pU = 0; o.pD = 1; ph0 = 2; ph1 = 3;
   } else {
@@ -83,37 +89,49 @@ __device__ __forceinline__ double2 pick(int p, double2 a0, double2 a1, double2 a
   return r;
 }
 
-// slot -> direction for the conversions
-__device__ __forceinline__ void slot_dirs(int x, int y, int nx, int ny, int d[4]) {
+// slot -> direction (D=0, L=1, R=2, U=3) for the conversions
+__device__ __forceinline__ void slot_dirs(int x, int gy, int nx, int ny, int d[4]) {
   const bool xe = (x == 0) | (x == nx - 1);
-  const int h0 = xe ? 2 : 1, h1 = xe ? 1 : 2;  // L=1, R=2
-  if (y == 0) {
+  const int h0 = xe ? 2 : 1, h1 = xe ? 1 : 2;
+  if (gy == 0) {
     d[0] = h0; d[1] = h1; d[2] = 3; d[3] = 0;
-  } else if (y == ny - 1) {
+  } else if (gy == ny - 1) {
     d[0] = 3; d[1] = 0; d[2] = h0; d[3] = h1;
   } else {
     d[0] = 0; d[1] = h0; d[2] = h1; d[3] = 3;
   }
 }
 
+__device__ __forceinline__ int global_row(const Geom& g, int ly) {
+  int gy = g.gy0 + ly;
+  if (gy >= g.ny) gy -= g.ny;
+  return gy;
+}
+
 template <int SHIFT, bool MARKED, bool PROB, bool TRACE>
 __global__ void __launch_bounds__(256)
-lattice_step_kernel(int nx, int ny, const double2* __restrict__ in, double2* __restrict__ out,
-                    const uint32_t* __restrict__ bits, double* __restrict__ prob, TraceArgs tr) {
+lattice_step_kernel(Geom g, Rows rows, const double2* __restrict__ in, double2* __restrict__ out,
+                    const uint32_t* __restrict__ bits, double* __restrict__ prob, int prob_row0,
+                    TraceArgs tr) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= nx) return;
-  const int64_t n = (int64_t)nx * ny;
-  for (int y = blockIdx.y; y < ny; y += gridDim.y) {
-    const int64_t w = (int64_t)y * nx + x;
+  if (x >= g.nx) return;
+  const int64_t P = g.pstride;
+  for (int r = blockIdx.y; r < rows.nrows; r += gridDim.y) {
+    const int ly = rows.row0 + r * rows.rstep;
+    const int gy = global_row(g, ly);
+    const int64_t w = (int64_t)ly * g.nx + x;
     const double2 vD = __ldcs(in + w);
-    const double2 vL = __ldcs(in + n + w);
-    const double2 vR = __ldcs(in + 2 * n + w);
-    const double2 vU = __ldcs(in + 3 * n + w);
-    const Slots o = order_slots(x, y, nx, ny, vD, vL, vR, vU);
+    const double2 vL = __ldcs(in + P + w);
+    const double2 vR = __ldcs(in + 2 * P + w);
+    const double2 vU = __ldcs(in + 3 * P + w);
+    const Slots o = order_slots(x, gy, g.nx, g.ny, vD, vL, vR, vU);
 
     double2 oD, oL, oR, oU;
     bool marked = false;
-    if (MARKED) marked = (__ldg(bits + (w >> 5)) >> (w & 31)) & 1u;
+    if (MARKED) {
+      const int64_t wg = (int64_t)gy * g.nx + x;
+      marked = (__ldg(bits + (wg >> 5)) >> (wg & 31)) & 1u;
+    }
     if (MARKED && marked) {
       oD = scale_np(-1.0, vD);
       oL = scale_np(-1.0, vL);
@@ -134,82 +152,120 @@ lattice_step_kernel(int nx, int ny, const double2* __restrict__ in, double2* __r
       oR = pick(o.pR, O0, O1, O2, O3);
       oU = pick(o.pU, O0, O1, O2, O3);
     }
-    const int ym = (y == 0) ? ny - 1 : y - 1;
-    const int yp = (y == ny - 1) ? 0 : y + 1;
-    const int xm = (x == 0) ? nx - 1 : x - 1;
-    const int xp = (x == nx - 1) ? 0 : x + 1;
-    const int64_t below = (int64_t)ym * nx + x, above = (int64_t)yp * nx + x;
-    const int64_t left = (int64_t)y * nx + xm, right = (int64_t)y * nx + xp;
+    int ym = ly - 1, yp = ly + 1;
+    if (g.wrap) {
+      ym = (ly == 0) ? g.lrows - 1 : ym;
+      yp = (ly == g.lrows - 1) ? 0 : yp;
+    }
+    const int xm = (x == 0) ? g.nx - 1 : x - 1;
+    const int xp = (x == g.nx - 1) ? 0 : x + 1;
+    const int64_t below = (int64_t)ym * g.nx + x, above = (int64_t)yp * g.nx + x;
+    const int64_t left = (int64_t)ly * g.nx + xm, right = (int64_t)ly * g.nx + xp;
     if (SHIFT == QWB_SHIFT_FLIPFLOP) {
-      __stcs(out + 3 * n + below, oD);   // arc (below -> w) points up
-      __stcs(out + 2 * n + left, oL);    // arc (left  -> w) points right
-      __stcs(out + 1 * n + right, oR);   // arc (right -> w) points left
-      __stcs(out + 0 * n + above, oU);   // arc (above -> w) points down
+      __stcs(out + 3 * P + below, oD);   // arc (below -> w) points up
+      __stcs(out + 2 * P + left, oL);    // arc (left  -> w) points right
+      __stcs(out + 1 * P + right, oR);   // arc (right -> w) points left
+      __stcs(out + 0 * P + above, oU);   // arc (above -> w) points down
     } else {
-      __stcs(out + 0 * n + below, oD);
-      __stcs(out + 1 * n + left, oL);
-      __stcs(out + 2 * n + right, oR);
-      __stcs(out + 3 * n + above, oU);
+      __stcs(out + 0 * P + below, oD);
+      __stcs(out + 1 * P + left, oL);
+      __stcs(out + 2 * P + right, oR);
+      __stcs(out + 3 * P + above, oU);
     }
     if (PROB || TRACE) {
       const double m0 = abs2_np(o.s0), m1 = abs2_np(o.s1), m2 = abs2_np(o.s2), m3 = abs2_np(o.s3);
       const double p = __dadd_rn(m0, __dadd_rn(__dadd_rn(m1, m2), m3));
-      if (PROB) __stcs(prob + w, p);
+      if (PROB) __stcs(prob + (int64_t)(ly - prob_row0) * g.nx + x, p);
       if (TRACE) {
+        const int64_t wg = (int64_t)gy * g.nx + x;
 #pragma unroll
         for (int j = 0; j < kMaxTrace; ++j)
-          if (j < tr.n && tr.v[j] == w) tr.out[j] = p;
+          if (j < tr.n && tr.v[j] == wg) tr.out[j] = p;
       }
     }
   }
 }
 
-__global__ void to_planes_kernel(int nx, int ny, const double2* __restrict__ arcs,
+// arcs (reference order, owned rows only, contiguous) <-> planes
+__global__ void to_planes_kernel(Geom g, int ly0, int nrows, const double2* __restrict__ arcs,
                                  double2* __restrict__ planes) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= nx) return;
-  const int64_t n = (int64_t)nx * ny;
-  for (int y = blockIdx.y; y < ny; y += gridDim.y) {
-    const int64_t w = (int64_t)y * nx + x;
+  if (x >= g.nx) return;
+  for (int r = blockIdx.y; r < nrows; r += gridDim.y) {
+    const int ly = ly0 + r;
+    const int64_t w = (int64_t)ly * g.nx + x;
+    const int64_t a = (int64_t)r * g.nx + x;
     int d[4];
-    slot_dirs(x, y, nx, ny, d);
+    slot_dirs(x, global_row(g, ly), g.nx, g.ny, d);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) planes[d[i] * n + w] = arcs[4 * w + i];
+    for (int i = 0; i < 4; ++i) planes[d[i] * g.pstride + w] = arcs[4 * a + i];
   }
 }
 
-__global__ void from_planes_kernel(int nx, int ny, const double2* __restrict__ planes,
+__global__ void from_planes_kernel(Geom g, int ly0, int nrows, const double2* __restrict__ planes,
                                    double2* __restrict__ arcs) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= nx) return;
-  const int64_t n = (int64_t)nx * ny;
-  for (int y = blockIdx.y; y < ny; y += gridDim.y) {
-    const int64_t w = (int64_t)y * nx + x;
+  if (x >= g.nx) return;
+  for (int r = blockIdx.y; r < nrows; r += gridDim.y) {
+    const int ly = ly0 + r;
+    const int64_t w = (int64_t)ly * g.nx + x;
+    const int64_t a = (int64_t)r * g.nx + x;
     int d[4];
-    slot_dirs(x, y, nx, ny, d);
+    slot_dirs(x, global_row(g, ly), g.nx, g.ny, d);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) arcs[4 * w + i] = planes[d[i] * n + w];
+    for (int i = 0; i < 4; ++i) arcs[4 * a + i] = planes[d[i] * g.pstride + w];
   }
 }
 
-__global__ void lattice_prob_kernel(int nx, int ny, const double2* __restrict__ planes,
+__global__ void lattice_prob_kernel(Geom g, int ly0, int nrows, const double2* __restrict__ planes,
                                     double* __restrict__ p) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= nx) return;
-  const int64_t n = (int64_t)nx * ny;
-  for (int y = blockIdx.y; y < ny; y += gridDim.y) {
-    const int64_t w = (int64_t)y * nx + x;
-    const Slots o = order_slots(x, y, nx, ny, planes[w], planes[n + w], planes[2 * n + w],
-                                planes[3 * n + w]);
+  if (x >= g.nx) return;
+  const int64_t P = g.pstride;
+  for (int r = blockIdx.y; r < nrows; r += gridDim.y) {
+    const int ly = ly0 + r;
+    const int64_t w = (int64_t)ly * g.nx + x;
+    const Slots o = order_slots(x, global_row(g, ly), g.nx, g.ny, planes[w], planes[P + w],
+                                planes[2 * P + w], planes[3 * P + w]);
     const double m0 = abs2_np(o.s0), m1 = abs2_np(o.s1), m2 = abs2_np(o.s2), m3 = abs2_np(o.s3);
-    p[w] = __dadd_rn(m0, __dadd_rn(__dadd_rn(m1, m2), m3));
+    p[(int64_t)r * g.nx + x] = __dadd_rn(m0, __dadd_rn(__dadd_rn(m1, m2), m3));
   }
 }
 
-dim3 lattice_grid(int64_t nx, int64_t ny) {
+dim3 grid_for(int nx, int nrows) {
   const unsigned gx = (unsigned)((nx + 255) / 256);
-  const unsigned gy = (unsigned)(ny < 65535 ? ny : 65535);
+  const unsigned gy = (unsigned)(nrows < 65535 ? (nrows > 0 ? nrows : 1) : 65535);
   return dim3(gx, gy, 1);
+}
+
+template <int SHIFT, bool MARKED, bool PROB, bool TRACE>
+void launch_t(cudaStream_t s, const Geom& g, const Rows& r, const double2* in, double2* out,
+              const uint32_t* bits, double* prob, int prob_row0, const TraceArgs& tr) {
+  lattice_step_kernel<SHIFT, MARKED, PROB, TRACE><<<grid_for(g.nx, r.nrows), 256, 0, s>>>(
+      g, r, in, out, bits, prob, prob_row0, tr);
+}
+
+template <int SHIFT>
+void launch_s(cudaStream_t s, const Geom& g, const Rows& r, const double2* in, double2* out,
+              const uint32_t* bits, double* prob, int prob_row0, const TraceArgs& tr) {
+  const bool m = bits != nullptr, p = prob != nullptr, t = tr.n > 0 && tr.out != nullptr;
+  if (m) {
+    if (p) {
+      if (t) launch_t<SHIFT, true, true, true>(s, g, r, in, out, bits, prob, prob_row0, tr);
+      else   launch_t<SHIFT, true, true, false>(s, g, r, in, out, bits, prob, prob_row0, tr);
+    } else {
+      if (t) launch_t<SHIFT, true, false, true>(s, g, r, in, out, bits, prob, prob_row0, tr);
+      else   launch_t<SHIFT, true, false, false>(s, g, r, in, out, bits, prob, prob_row0, tr);
+    }
+  } else {
+    if (p) {
+      if (t) launch_t<SHIFT, false, true, true>(s, g, r, in, out, bits, prob, prob_row0, tr);
+      else   launch_t<SHIFT, false, true, false>(s, g, r, in, out, bits, prob, prob_row0, tr);
+    } else {
+      if (t) launch_t<SHIFT, false, false, true>(s, g, r, in, out, bits, prob, prob_row0, tr);
+      else   launch_t<SHIFT, false, false, false>(s, g, r, in, out, bits, prob, prob_row0, tr);
+    }
+  }
 }
 
 int check_dims(qwb_ctx* ctx, int64_t nx, int64_t ny) {
@@ -221,44 +277,60 @@ int check_dims(qwb_ctx* ctx, int64_t nx, int64_t ny) {
   return QWB_OK;
 }
 
-template <int SHIFT, bool MARKED, bool PROB, bool TRACE>
-void launch_step_t(dim3 g, cudaStream_t s, int nx, int ny, const double2* in, double2* out,
-                   const uint32_t* bits, double* prob, const TraceArgs& tr) {
-  lattice_step_kernel<SHIFT, MARKED, PROB, TRACE><<<g, 256, 0, s>>>(nx, ny, in, out, bits, prob, tr);
-}
-
-template <int SHIFT>
-void launch_step_s(dim3 g, cudaStream_t s, int nx, int ny, const double2* in, double2* out,
-                   const uint32_t* bits, double* prob, const TraceArgs& tr) {
-  const bool m = bits != nullptr, p = prob != nullptr, t = tr.n > 0 && tr.out != nullptr;
-  if (m) {
-    if (p) {
-      if (t) launch_step_t<SHIFT, true, true, true>(g, s, nx, ny, in, out, bits, prob, tr);
-      else   launch_step_t<SHIFT, true, true, false>(g, s, nx, ny, in, out, bits, prob, tr);
-    } else {
-      if (t) launch_step_t<SHIFT, true, false, true>(g, s, nx, ny, in, out, bits, prob, tr);
-      else   launch_step_t<SHIFT, true, false, false>(g, s, nx, ny, in, out, bits, prob, tr);
-    }
-  } else {
-    if (p) {
-      if (t) launch_step_t<SHIFT, false, true, true>(g, s, nx, ny, in, out, bits, prob, tr);
-      else   launch_step_t<SHIFT, false, true, false>(g, s, nx, ny, in, out, bits, prob, tr);
-    } else {
-      if (t) launch_step_t<SHIFT, false, false, true>(g, s, nx, ny, in, out, bits, prob, tr);
-      else   launch_step_t<SHIFT, false, false, false>(g, s, nx, ny, in, out, bits, prob, tr);
-    }
-  }
-}
-
-void launch_step(int shift, dim3 g, cudaStream_t s, int nx, int ny, const double2* in,
-                 double2* out, const uint32_t* bits, double* prob, const TraceArgs& tr) {
-  if (shift == QWB_SHIFT_FLIPFLOP)
-    launch_step_s<QWB_SHIFT_FLIPFLOP>(g, s, nx, ny, in, out, bits, prob, tr);
-  else
-    launch_step_s<QWB_SHIFT_PERSISTENT>(g, s, nx, ny, in, out, bits, prob, tr);
+Geom single_geom(int64_t nx, int64_t ny) {
+  Geom g;
+  g.nx = (int)nx;
+  g.ny = (int)ny;
+  g.lrows = (int)ny;
+  g.gy0 = 0;
+  g.wrap = 1;
+  g.pstride = nx * ny;
+  return g;
 }
 
 }  // namespace
+
+namespace qwb {
+
+void lattice_launch(int shift, cudaStream_t s, const Geom& g, const Rows& r, const double2* in,
+                    double2* out, const uint32_t* bits, double* prob, int prob_row0,
+                    const TraceArgs& tr) {
+  if (r.nrows <= 0) return;
+  if (shift == QWB_SHIFT_FLIPFLOP)
+    launch_s<QWB_SHIFT_FLIPFLOP>(s, g, r, in, out, bits, prob, prob_row0, tr);
+  else
+    launch_s<QWB_SHIFT_PERSISTENT>(s, g, r, in, out, bits, prob, prob_row0, tr);
+}
+
+int lattice_check_shift(qwb_ctx* ctx, int shift) {
+  if (shift != QWB_SHIFT_FLIPFLOP && shift != QWB_SHIFT_PERSISTENT)
+    QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "shift: unknown shift code %d", shift);
+  return QWB_OK;
+}
+
+int lattice_slab_geom(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, Geom* g) {
+  int st = check_dims(ctx, nx, ny);
+  if (st) return st;
+  if (ny_local < 2 || y0 < 0 || y0 + ny_local > ny)
+    QWB_FAIL(ctx, QWB_E_DIMENSION, "slab rows [%lld, %lld) invalid for ny=%lld (need >= 2 rows)",
+             (long long)y0, (long long)(y0 + ny_local), (long long)ny);
+  g->nx = (int)nx;
+  g->ny = (int)ny;
+  g->lrows = (int)(ny_local + 2);
+  g->gy0 = (int)((y0 - 1 + ny) % ny);
+  g->wrap = 0;
+  g->pstride = nx * (ny_local + 2);
+  return QWB_OK;
+}
+
+Rows slab_rows(int64_t ny_local, int part) {
+  const int nl = (int)ny_local;
+  if (part == 1) return Rows{1, nl - 1, 2};
+  if (part == 2) return Rows{2, 1, nl - 2};
+  return Rows{1, 1, nl};
+}
+
+}  // namespace qwb
 
 extern "C" {
 
@@ -267,8 +339,9 @@ int qwb_lattice_to_planes(qwb_ctx* ctx, int64_t nx, int64_t ny, const qwb_z* arc
   QWB_BEGIN(ctx);
   int st = check_dims(ctx, nx, ny);
   if (st) return st;
-  to_planes_kernel<<<lattice_grid(nx, ny), 256, 0, qwb::as_stream(stream)>>>(
-      (int)nx, (int)ny, reinterpret_cast<const double2*>(arcs), reinterpret_cast<double2*>(planes));
+  const Geom g = single_geom(nx, ny);
+  to_planes_kernel<<<grid_for(g.nx, g.ny), 256, 0, qwb::as_stream(stream)>>>(
+      g, 0, g.ny, reinterpret_cast<const double2*>(arcs), reinterpret_cast<double2*>(planes));
   QWB_LAUNCH_CHECK(ctx, "to_planes_kernel");
   return QWB_OK;
 }
@@ -278,8 +351,9 @@ int qwb_lattice_from_planes(qwb_ctx* ctx, int64_t nx, int64_t ny, const qwb_z* p
   QWB_BEGIN(ctx);
   int st = check_dims(ctx, nx, ny);
   if (st) return st;
-  from_planes_kernel<<<lattice_grid(nx, ny), 256, 0, qwb::as_stream(stream)>>>(
-      (int)nx, (int)ny, reinterpret_cast<const double2*>(planes), reinterpret_cast<double2*>(arcs));
+  const Geom g = single_geom(nx, ny);
+  from_planes_kernel<<<grid_for(g.nx, g.ny), 256, 0, qwb::as_stream(stream)>>>(
+      g, 0, g.ny, reinterpret_cast<const double2*>(planes), reinterpret_cast<double2*>(arcs));
   QWB_LAUNCH_CHECK(ctx, "from_planes_kernel");
   return QWB_OK;
 }
@@ -288,15 +362,13 @@ int qwb_lattice_step(qwb_ctx* ctx, int64_t nx, int64_t ny, int shift, const uint
                      const qwb_z* in, qwb_z* out, double* prob_in, void* stream) {
   QWB_BEGIN(ctx);
   int st = check_dims(ctx, nx, ny);
+  if (!st) st = qwb::lattice_check_shift(ctx, shift);
   if (st) return st;
-  if (shift != QWB_SHIFT_FLIPFLOP && shift != QWB_SHIFT_PERSISTENT)
-    QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "shift: unknown shift code %d", shift);
   TraceArgs tr{};
-  tr.n = 0;
-  tr.out = nullptr;
-  launch_step(shift, lattice_grid(nx, ny), qwb::as_stream(stream), (int)nx, (int)ny,
-              reinterpret_cast<const double2*>(in), reinterpret_cast<double2*>(out), marked_bits,
-              prob_in, tr);
+  const Geom g = single_geom(nx, ny);
+  const Rows r{0, 1, g.ny};
+  qwb::lattice_launch(shift, qwb::as_stream(stream), g, r, reinterpret_cast<const double2*>(in),
+                      reinterpret_cast<double2*>(out), marked_bits, prob_in, 0, tr);
   QWB_LAUNCH_CHECK(ctx, "lattice_step_kernel");
   return QWB_OK;
 }
@@ -306,9 +378,8 @@ int qwb_lattice_run(qwb_ctx* ctx, int64_t nx, int64_t ny, int shift, const uint3
                     int n_trace, double* trace, int* final_in_b_host, void* stream) {
   QWB_BEGIN(ctx);
   int st = check_dims(ctx, nx, ny);
+  if (!st) st = qwb::lattice_check_shift(ctx, shift);
   if (st) return st;
-  if (shift != QWB_SHIFT_FLIPFLOP && shift != QWB_SHIFT_PERSISTENT)
-    QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "shift: unknown shift code %d", shift);
   if (steps < 0) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "steps must be >= 0");
   if (n_trace < 0 || n_trace > kMaxTrace)
     QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "at most %d trace vertices", kMaxTrace);
@@ -320,12 +391,13 @@ int qwb_lattice_run(qwb_ctx* ctx, int64_t nx, int64_t ny, int shift, const uint3
       QWB_FAIL(ctx, QWB_E_MARKED_OUT_OF_RANGE, "trace vertex %lld out of range", (long long)tr.v[j]);
   }
   cudaStream_t s = qwb::as_stream(stream);
-  const dim3 g = lattice_grid(nx, ny);
+  const Geom g = single_geom(nx, ny);
+  const Rows r{0, 1, g.ny};
   double2* cur = reinterpret_cast<double2*>(a);
   double2* nxt = reinterpret_cast<double2*>(b);
   for (int64_t k = 0; k < steps; ++k) {
     tr.out = trace ? trace + k * n_trace : nullptr;
-    launch_step(shift, g, s, (int)nx, (int)ny, cur, nxt, marked_bits, nullptr, tr);
+    qwb::lattice_launch(shift, s, g, r, cur, nxt, marked_bits, nullptr, 0, tr);
     double2* t = cur;
     cur = nxt;
     nxt = t;
@@ -340,9 +412,64 @@ int qwb_lattice_probability(qwb_ctx* ctx, int64_t nx, int64_t ny, const qwb_z* p
   QWB_BEGIN(ctx);
   int st = check_dims(ctx, nx, ny);
   if (st) return st;
-  lattice_prob_kernel<<<lattice_grid(nx, ny), 256, 0, qwb::as_stream(stream)>>>(
-      (int)nx, (int)ny, reinterpret_cast<const double2*>(planes), p);
+  const Geom g = single_geom(nx, ny);
+  lattice_prob_kernel<<<grid_for(g.nx, g.ny), 256, 0, qwb::as_stream(stream)>>>(
+      g, 0, g.ny, reinterpret_cast<const double2*>(planes), p);
   QWB_LAUNCH_CHECK(ctx, "lattice_prob_kernel");
+  return QWB_OK;
+}
+
+// ---- slabs (one rank's rows of a sharded torus) ----------------------------
+
+int qwb_slab_to_planes(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local,
+                       const qwb_z* arcs, qwb_z* planes, void* stream) {
+  QWB_BEGIN(ctx);
+  Geom g;
+  int st = qwb::lattice_slab_geom(ctx, nx, ny, y0, ny_local, &g);
+  if (st) return st;
+  to_planes_kernel<<<grid_for(g.nx, (int)ny_local), 256, 0, qwb::as_stream(stream)>>>(
+      g, 1, (int)ny_local, reinterpret_cast<const double2*>(arcs), reinterpret_cast<double2*>(planes));
+  QWB_LAUNCH_CHECK(ctx, "to_planes_kernel(slab)");
+  return QWB_OK;
+}
+
+int qwb_slab_from_planes(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local,
+                         const qwb_z* planes, qwb_z* arcs, void* stream) {
+  QWB_BEGIN(ctx);
+  Geom g;
+  int st = qwb::lattice_slab_geom(ctx, nx, ny, y0, ny_local, &g);
+  if (st) return st;
+  from_planes_kernel<<<grid_for(g.nx, (int)ny_local), 256, 0, qwb::as_stream(stream)>>>(
+      g, 1, (int)ny_local, reinterpret_cast<const double2*>(planes), reinterpret_cast<double2*>(arcs));
+  QWB_LAUNCH_CHECK(ctx, "from_planes_kernel(slab)");
+  return QWB_OK;
+}
+
+int qwb_slab_probability(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local,
+                         const qwb_z* planes, double* p, void* stream) {
+  QWB_BEGIN(ctx);
+  Geom g;
+  int st = qwb::lattice_slab_geom(ctx, nx, ny, y0, ny_local, &g);
+  if (st) return st;
+  lattice_prob_kernel<<<grid_for(g.nx, (int)ny_local), 256, 0, qwb::as_stream(stream)>>>(
+      g, 1, (int)ny_local, reinterpret_cast<const double2*>(planes), p);
+  QWB_LAUNCH_CHECK(ctx, "lattice_prob_kernel(slab)");
+  return QWB_OK;
+}
+
+int qwb_slab_step(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int shift,
+                  const uint32_t* marked_bits, const qwb_z* in, qwb_z* out, int part, void* stream) {
+  QWB_BEGIN(ctx);
+  Geom g;
+  int st = qwb::lattice_slab_geom(ctx, nx, ny, y0, ny_local, &g);
+  if (!st) st = qwb::lattice_check_shift(ctx, shift);
+  if (st) return st;
+  if (part < 0 || part > 2) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "part must be 0, 1 or 2");
+  TraceArgs tr{};
+  qwb::lattice_launch(shift, qwb::as_stream(stream), g, qwb::slab_rows(ny_local, part),
+                      reinterpret_cast<const double2*>(in), reinterpret_cast<double2*>(out),
+                      marked_bits, nullptr, 0, tr);
+  QWB_LAUNCH_CHECK(ctx, "lattice_step_kernel(slab)");
   return QWB_OK;
 }
 

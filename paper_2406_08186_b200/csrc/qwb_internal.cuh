@@ -19,6 +19,11 @@ struct qwb_ctx {
   // pinned host staging for small readbacks
   void* pinned;
   std::string last_error;
+  // multi-GPU (comm.cu): NCCL communicator, its stream and ordering events
+  void* comm;
+  int nranks, rank;
+  cudaStream_t comm_stream;
+  cudaEvent_t ev_ready, ev_done;
 };
 
 namespace qwb {

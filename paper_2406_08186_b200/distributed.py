@@ -1,0 +1,170 @@
+"""Multi-GPU coined walk: one periodic lattice split into y-slabs, one per rank.
+
+No reference counterpart (the reference's only parallelism is the in-process
+row-block pool, backend.py:426-430; multi-GPU is future work).
+
+Plumbing: one process per GPU (torchrun), `torch.distributed` only to agree on
+the NCCL unique id; the per-step halo exchange runs inside libqwb200
+(`qwb_slab_run`: NCCL send/recv of two nx-long rows on a comm stream,
+overlapped with the interior rows).  Results are bitwise equal to the
+single-GPU run because every arc is computed with the same formula and the
+position classes use global coordinates.
+
+The plan (`slab_partition`, `neighbours`) is plain Python so it is tested on
+CPU with the gloo backend (tests/test_distributed_cpu.py).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import _native as N
+from .backend import Engine, empty_z
+from .errors import DimensionMismatch
+
+
+def slab_partition(ny: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous, balanced y-slabs [(y0, rows)], every slab >= 2 rows."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    if ny < 2 * world:
+        raise DimensionMismatch(f"ny={ny} too small for {world} slabs of >= 2 rows")
+    base, extra = divmod(ny, world)
+    out, y = [], 0
+    for r in range(world):
+        rows = base + (1 if r < extra else 0)
+        out.append((y, rows))
+        y += rows
+    return out
+
+
+def neighbours(rank: int, world: int) -> tuple[int, int]:
+    """(rank below, rank above) on the periodic y ring."""
+    return (rank - 1) % world, (rank + 1) % world
+
+
+def owned_arc_range(nx: int, y0: int, rows: int) -> tuple[int, int]:
+    """Arcs of rows [y0, y0+rows) in the reference order: contiguous, 4 per vertex."""
+    return 4 * nx * y0, 4 * nx * (y0 + rows)
+
+
+def _nccl_path() -> str | None:
+    try:
+        import nvidia.nccl
+        for base in list(getattr(nvidia.nccl, "__path__", [])):
+            p = os.path.join(base, "lib", "libnccl.so.2")
+            if os.path.exists(p):
+                return p
+    except Exception:
+        pass
+    return None
+
+
+class SlabLattice:
+    """This rank's slab of a periodic nx x ny lattice walk (flip-flop or
+    persistent shift, optional marked vertices).  Call collectively."""
+
+    def __init__(self, engine: Engine, nx: int, ny: int, shift: str = "flipflop", marked=(),
+                 rank: int = 0, world: int = 1, group=None):
+        import torch
+        import torch.distributed as dist
+        self.engine = engine
+        self.nx, self.ny = int(nx), int(ny)
+        self.rank, self.world = int(rank), int(world)
+        self.y0, self.rows = slab_partition(self.ny, self.world)[self.rank]
+        self.below, self.above = neighbours(self.rank, self.world)
+        self.shift = N.SHIFT[shift]
+        self.bits = None
+        if marked:
+            n = self.nx * self.ny
+            self.bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=engine.torch_device)
+            mk = torch.tensor(sorted(int(v) for v in marked), dtype=torch.int64, device=engine.torch_device)
+            engine.call("qwb_marked_bitmap", n, N.ptr(mk), len(marked), N.ptr(self.bits), engine.stream())
+        size = 4 * self.nx * (self.rows + 2)
+        self.a = empty_z(engine, size)
+        self.b = empty_z(engine, size)
+        self.a.zero_()
+        self.b.zero_()
+        if self.world > 1:
+            lib = N.load()
+            path = _nccl_path()
+            if path and not os.environ.get("QWB_NCCL_LIB"):
+                os.environ["QWB_NCCL_LIB"] = path
+            uid = C.create_string_buffer(128)
+            if self.rank == 0:
+                N.check(lib.qwb_comm_unique_id(uid))
+            obj = [uid.raw if self.rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            uid = C.create_string_buffer(obj[0], 128)
+            engine.call("qwb_comm_init", uid, self.world, self.rank)
+
+    def load(self, owned_arcs) -> None:
+        """owned_arcs: device tensor of this slab's arcs (reference order)."""
+        self.engine.call("qwb_slab_to_planes", self.nx, self.ny, self.y0, self.rows, N.ptr(owned_arcs),
+                         N.ptr(self.a), self.engine.stream())
+
+    def advance(self, steps: int) -> None:
+        if steps <= 0:
+            return
+        eng = self.engine
+        if self.world == 1:
+            raise RuntimeError("use the single-GPU lattice path for world == 1")
+        flag = C.c_int(0)
+        eng.call("qwb_slab_run", self.nx, self.ny, self.y0, self.rows, self.shift, N.ptr(self.bits),
+                 N.ptr(self.a), N.ptr(self.b), int(steps), self.below, self.above, C.byref(flag),
+                 eng.stream())
+        if flag.value:
+            self.a, self.b = self.b, self.a
+
+    def store(self, owned_arcs) -> None:
+        self.engine.call("qwb_slab_from_planes", self.nx, self.ny, self.y0, self.rows, N.ptr(self.a),
+                         N.ptr(owned_arcs), self.engine.stream())
+
+    def probability(self, p) -> None:
+        self.engine.call("qwb_slab_probability", self.nx, self.ny, self.y0, self.rows, N.ptr(self.a),
+                         N.ptr(p), self.engine.stream())
+
+    def close(self) -> None:
+        if self.world > 1:
+            self.engine.call("qwb_comm_destroy")
+
+
+def emulate_slabs(engine: Engine, nx: int, ny: int, world: int, psi_arcs: np.ndarray, steps: int,
+                  shift: str = "flipflop", marked=()):
+    """Run the slab decomposition for `world` slabs on ONE device (slab kernel
+    + the same two-row exchange as qwb_slab_run, done with device copies) and
+    return the full arc state.  Test hook for the multi-GPU path."""
+    import torch
+    parts = slab_partition(ny, world)
+    sh = N.SHIFT[shift]
+    bits = None
+    if marked:
+        n = nx * ny
+        bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=engine.torch_device)
+        mk = torch.tensor(sorted(marked), dtype=torch.int64, device=engine.torch_device)
+        engine.call("qwb_marked_bitmap", n, N.ptr(mk), len(marked), N.ptr(bits), engine.stream())
+    full = torch.from_numpy(np.ascontiguousarray(psi_arcs)).to(engine.torch_device)
+    cur, nxt = [], []
+    for (y0, rows) in parts:
+        a = empty_z(engine, 4 * nx * (rows + 2)).zero_()
+        b = empty_z(engine, 4 * nx * (rows + 2)).zero_()
+        lo, hi = owned_arc_range(nx, y0, rows)
+        engine.call("qwb_slab_to_planes", nx, ny, y0, rows, N.ptr(full[lo:hi]), N.ptr(a), engine.stream())
+        cur.append(a)
+        nxt.append(b)
+    nl = N.i64_array([r for (_, r) in parts])
+    for _ in range(steps):
+        for i, (y0, rows) in enumerate(parts):
+            engine.call("qwb_slab_step", nx, ny, y0, rows, sh, N.ptr(bits), N.ptr(cur[i]), N.ptr(nxt[i]), 0,
+                        engine.stream())
+        ptrs = (C.c_void_p * world)(*[N.ptr(t) for t in nxt])
+        engine.call("qwb_slab_exchange_local", nx, sh, nl, ptrs, world, engine.stream())
+        cur, nxt = nxt, cur
+    out = torch.empty_like(full)
+    for i, (y0, rows) in enumerate(parts):
+        lo, hi = owned_arc_range(nx, y0, rows)
+        engine.call("qwb_slab_from_planes", nx, ny, y0, rows, N.ptr(cur[i]), N.ptr(out[lo:hi]), engine.stream())
+    return out.cpu().numpy()

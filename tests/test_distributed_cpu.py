@@ -1,0 +1,124 @@
+"""Multi-GPU decomposition checked on CPU.
+
+1. The numpy model of the plane-layout step (tests/planes_model.py) equals the
+   reference CSR step bitwise (so the model is a valid stand-in for the kernel).
+2. The slab plan (paper_2406_08186_b200.distributed.slab_partition /
+   neighbours) + the per-step two-row exchange reproduces the unsharded walk
+   bitwise, with real processes exchanging rows over torch.distributed gloo
+   (world sizes 2 and 3).  The GPU path runs the same plan with NCCL.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import planes_model as PM
+from oracle import qwalk_oracle as O
+from paper_2406_08186_b200 import distributed as DI
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _psi(n, seed):
+    rng = np.random.default_rng(seed)
+    v = rng.normal(size=n) + 1j * rng.normal(size=n)
+    return v / np.linalg.norm(v)
+
+
+@pytest.mark.parametrize("nx,ny,shift,marked", [(5, 5, "flipflop", ()), (7, 4, "persistent", (9,)),
+                                                 (16, 12, "flipflop", (0, 37, 191)), (3, 3, "persistent", ())])
+def test_planes_model_equals_reference_step(nx, ny, shift, marked):
+    offs, cols = O.grid_adjacency(nx, ny)
+    u = O.evolution_operator(offs, cols, shift, marked, "grid", (nx, ny, True))
+    psi = _psi(4 * nx * ny, nx * ny)
+    ref = O.coined_simulate(u, psi, [9])[0]
+    got = PM.run_full(nx, ny, psi, 9, shift, marked)
+    assert np.array_equal(got, ref)
+
+
+def test_partition_plan():
+    for ny, w in ((8, 2), (9, 2), (2048, 8), (10, 3), (6, 3)):
+        parts = DI.slab_partition(ny, w)
+        assert sum(r for _, r in parts) == ny
+        assert all(r >= 2 for _, r in parts)
+        assert [y for y, _ in parts] == list(np.cumsum([0] + [r for _, r in parts])[:-1])
+        assert max(r for _, r in parts) - min(r for _, r in parts) <= 1
+    assert DI.neighbours(0, 4) == (3, 1)
+    assert DI.neighbours(3, 4) == (2, 0)
+    with pytest.raises(Exception):
+        DI.slab_partition(5, 3)
+    assert DI.owned_arc_range(10, 2, 3) == (80, 200)
+
+
+def test_slabs_single_process_equal_full():
+    nx, ny = 6, 9
+    psi = _psi(4 * nx * ny, 1)
+    for shift in ("flipflop", "persistent"):
+        full = PM.run_full(nx, ny, psi, 7, shift, (13,))
+        for w in (2, 3, 4):
+            parts = DI.slab_partition(ny, w)
+            slabs = []
+            for (y0, rows) in parts:
+                lo, hi = DI.owned_arc_range(nx, y0, rows)
+                slabs.append(PM.arcs_to_planes(nx, ny, psi[lo:hi], y0, rows, extra=1))
+            for _ in range(7):
+                slabs = [PM.step_slab(nx, ny, y0, rows, s, shift, (13,)) for s, (y0, rows) in zip(slabs, parts)]
+                PM.exchange_local(slabs, shift)
+            got = np.concatenate([PM.planes_to_arcs(nx, ny, s, y0, rows, extra=1)
+                                  for s, (y0, rows) in zip(slabs, parts)])
+            assert np.array_equal(got, full), (shift, w)
+
+
+def _worker(rank, world, port, nx, ny, steps, shift, marked, out_dir):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    psi = _psi(4 * nx * ny, 3)
+    y0, rows = DI.slab_partition(ny, world)[rank]
+    below, above = DI.neighbours(rank, world)
+    pd, pu = PM.edge_planes(shift)
+    lo, hi = DI.owned_arc_range(nx, y0, rows)
+    planes = PM.arcs_to_planes(nx, ny, psi[lo:hi], y0, rows, extra=1)
+    for _ in range(steps):
+        planes = PM.step_slab(nx, ny, y0, rows, planes, shift, marked)
+        # same pairing as comm.cu's NCCL group: send down / recv from up / send up / recv from down
+        send_down = torch.from_numpy(planes[pd, 0, :].copy())
+        send_up = torch.from_numpy(planes[pu, rows + 1, :].copy())
+        recv_up = torch.empty_like(send_down)
+        recv_down = torch.empty_like(send_up)
+        ops = [dist.P2POp(dist.isend, send_down, below), dist.P2POp(dist.irecv, recv_up, above),
+               dist.P2POp(dist.isend, send_up, above), dist.P2POp(dist.irecv, recv_down, below)]
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+        planes[pd, rows, :] = recv_up.numpy()
+        planes[pu, 1, :] = recv_down.numpy()
+    local = PM.planes_to_arcs(nx, ny, planes, y0, rows, extra=1)
+    np.save(os.path.join(out_dir, f"slab{rank}.npy"), local)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,shift", [(2, "flipflop"), (3, "persistent"), (2, "persistent")])
+def test_gloo_multiprocess_halo_exchange(tmp_path, world, shift):
+    import torch.multiprocessing as mp
+    nx, ny, steps, marked = 8, 10, 6, (17, 44)
+    port = _free_port()
+    mp.start_processes(_worker, args=(world, port, nx, ny, steps, shift, marked, str(tmp_path)),
+                       nprocs=world, join=True, start_method="spawn")
+    got = np.concatenate([np.load(tmp_path / f"slab{r}.npy") for r in range(world)])
+    offs, cols = O.grid_adjacency(nx, ny)
+    u = O.evolution_operator(offs, cols, shift, marked, "grid", (nx, ny, True))
+    ref = O.coined_simulate(u, _psi(4 * nx * ny, 3), [steps])[0]
+    assert np.array_equal(got, ref)
