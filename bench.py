@@ -434,6 +434,49 @@ def measure_extras(q, CO, eng, dev, peak):
     out["csr_spmv_grid2048"] = {"arc_updates_per_s": n / per, "achieved_GBps": gbs, "frac": gbs / peak,
                                 "bytes_per_arc": csr_bytes, "us_per_step": per * 1e6,
                                 "device_build_s": build_s}
+    del u, xa, xb
+    torch.cuda.empty_cache()
+
+    # C1: cycle(1024), all 501 snapshots through the public API (one persistent CTA)
+    g = q.graphs.cycle(1024)
+    b = q.graphs.arc_basis(g)
+    amp = np.zeros(b.size, complex)
+    amp[q.graphs.arc_index(b, 512, 513)] = 1 / np.sqrt(2)
+    amp[q.graphs.arc_index(b, 512, 511)] = 1j / np.sqrt(2)
+    st0 = q.WalkState(b, amp)
+    spec = q.CoinedSpec(g)
+    CO.simulate(eng, spec, (0, 501, 1), st0)
+    t0 = time.perf_counter()
+    reps = 5
+    for _ in range(reps):
+        CO.simulate(eng, spec, (0, 501, 1), st0)
+    dt = (time.perf_counter() - t0) / reps
+    out["c1_cycle1024_500steps"] = {"seconds_per_simulate": dt, "arc_updates_per_s": 2048 * 500 / dt,
+                                    "note": "wall time of coined.simulate(range (0,501,1)) incl. U build, "
+                                            "H2D, 500 steps, D2H of 501 snapshots"}
+
+    # C4: hypercube(22) CTQW, gamma = 1/22, marked {0}, one evolve of t = 1 (2 sub-steps)
+    dim = 22
+    hc = q.graphs.hypercube(dim)
+    cs = q.CtqwSpec(hc, 1.0 / dim, 1.0, frozenset({0}))
+    from paper_2406_08186_b200 import ctqw as CT
+    op = CT._Operator(eng, cs)
+    nv = 1 << dim
+    x = torch.full((nv,), 1.0 / np.sqrt(nv), dtype=torch.complex128, device=dev)
+    op.evolve(x, 1.0, 1e-12)
+    torch.cuda.synchronize(dev)
+    x.fill_(1.0 / np.sqrt(nv))
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    terms = op.evolve(x, 1.0, 1e-12)
+    torch.cuda.synchronize(dev)
+    dt = time.perf_counter() - t0
+    nterms = sum(terms)
+    out["c4_hypercube22_ctqw"] = {"seconds_per_evolve_t1": dt, "substeps": len(terms), "terms": terms,
+                                  "us_per_term": dt / nterms * 1e6,
+                                  "vertex_term_updates_per_s": nv * nterms / dt,
+                                  "achieved_GBps_64B_per_vertex_term": 64 * nv * nterms / dt / 1e9,
+                                  "inf_norm": op.inf_norm}
     return out
 
 

@@ -49,45 +49,10 @@ using qwb::kMaxTrace;
 using qwb::Rows;
 using qwb::TraceArgs;
 
-// numpy product (c + 0i) * a
-__device__ __forceinline__ double2 scale_np(double c, double2 a) {
-  return cmul_np(make_double2(c, 0.0), a);
-}
-
-struct Slots {
-  double2 s0, s1, s2, s3;   // amplitudes in reference slot order
-  int pD, pL, pR, pU;       // slot of each direction
-};
-
-__device__ __forceinline__ Slots order_slots(int x, int gy, int nx, int ny, double2 vD, double2 vL,
-                                             double2 vR, double2 vU) {
-  Slots o;
-  const bool xe = (x == 0) | (x == nx - 1);
-  const double2 h0 = xe ? vR : vL;
-  const double2 h1 = xe ? vL : vR;
-  int ph0, ph1;
-  if (gy == 0) {
-    o.s0 = h0; o.s1 = h1; o.s2 = vU; o.s3 = vD;
-    ph0 = 0; ph1 = 1; o.pU = 2; o.pD = 3;
-  } else if (gy == ny - 1) {
-    o.s0 = vU; o.s1 = vD; o.s2 = h0; o.s3 = h1;
-    o.pU = 0; o.pD = 1; ph0 = 2; ph1 = 3;
-  } else {
-    o.s0 = vD; o.s1 = h0; o.s2 = h1; o.s3 = vU;
-    o.pD = 0; ph0 = 1; ph1 = 2; o.pU = 3;
-  }
-  o.pL = xe ? ph1 : ph0;
-  o.pR = xe ? ph0 : ph1;
-  return o;
-}
-
-__device__ __forceinline__ double2 pick(int p, double2 a0, double2 a1, double2 a2, double2 a3) {
-  double2 r = a0;
-  r = (p == 1) ? a1 : r;
-  r = (p == 2) ? a2 : r;
-  r = (p == 3) ? a3 : r;
-  return r;
-}
+using qwb::order_slots;
+using qwb::pick;
+using qwb::scale_np;
+using qwb::Slots;
 
 // slot -> direction (D=0, L=1, R=2, U=3) for the conversions
 __device__ __forceinline__ void slot_dirs(int x, int gy, int nx, int ny, int d[4]) {
@@ -132,26 +97,7 @@ lattice_step_kernel(Geom g, Rows rows, const double2* __restrict__ in, double2* 
       const int64_t wg = (int64_t)gy * g.nx + x;
       marked = (__ldg(bits + (wg >> 5)) >> (wg & 31)) & 1u;
     }
-    if (MARKED && marked) {
-      oD = scale_np(-1.0, vD);
-      oL = scale_np(-1.0, vL);
-      oR = scale_np(-1.0, vR);
-      oU = scale_np(-1.0, vU);
-    } else {
-      const double2 q0 = scale_np(0.5, o.s0), q1 = scale_np(0.5, o.s1);
-      const double2 q2 = scale_np(0.5, o.s2), q3 = scale_np(0.5, o.s3);
-      const double2 n0 = scale_np(-0.5, o.s0), n1 = scale_np(-0.5, o.s1);
-      const double2 n2 = scale_np(-0.5, o.s2), n3 = scale_np(-0.5, o.s3);
-      const double2 t12 = cadd(q1, q2);
-      const double2 O0 = cadd(n0, cadd(t12, q3));
-      const double2 O1 = cadd(q0, cadd(cadd(n1, q2), q3));
-      const double2 O2 = cadd(q0, cadd(cadd(q1, n2), q3));
-      const double2 O3 = cadd(q0, cadd(t12, n3));
-      oD = pick(o.pD, O0, O1, O2, O3);
-      oL = pick(o.pL, O0, O1, O2, O3);
-      oR = pick(o.pR, O0, O1, O2, O3);
-      oU = pick(o.pU, O0, O1, O2, O3);
-    }
+    qwb::vertex_outputs(o, marked, vD, vL, vR, vU, oD, oL, oR, oU);
     int ym = ly - 1, yp = ly + 1;
     if (g.wrap) {
       ym = (ly == 0) ? g.lrows - 1 : ym;
@@ -395,15 +341,30 @@ int qwb_lattice_run(qwb_ctx* ctx, int64_t nx, int64_t ny, int shift, const uint3
   const Rows r{0, 1, g.ny};
   double2* cur = reinterpret_cast<double2*>(a);
   double2* nxt = reinterpret_cast<double2*>(b);
-  for (int64_t k = 0; k < steps; ++k) {
+  int swaps = 0;
+  int64_t k = 0;
+  // T coined steps per HBM pass when no per-step trace is requested
+  const int depth = trace ? 0 : qwb::lattice_tb_depth(nx, ny);
+  if (depth > 0) {
+    for (; k + depth <= steps; k += depth) {
+      st = qwb::lattice_tb_launch(ctx, depth, shift, s, (int)nx, (int)ny, cur, nxt, marked_bits);
+      if (st) return st;
+      double2* t = cur;
+      cur = nxt;
+      nxt = t;
+      ++swaps;
+    }
+  }
+  for (; k < steps; ++k) {
     tr.out = trace ? trace + k * n_trace : nullptr;
     qwb::lattice_launch(shift, s, g, r, cur, nxt, marked_bits, nullptr, 0, tr);
     double2* t = cur;
     cur = nxt;
     nxt = t;
+    ++swaps;
   }
-  QWB_LAUNCH_CHECK(ctx, "lattice_step_kernel");
-  if (final_in_b_host) *final_in_b_host = (steps % 2) ? 1 : 0;
+  QWB_LAUNCH_CHECK(ctx, "lattice kernels");
+  if (final_in_b_host) *final_in_b_host = swaps & 1;
   return QWB_OK;
 }
 

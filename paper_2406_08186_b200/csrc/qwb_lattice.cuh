@@ -26,10 +26,83 @@ struct Rows {
   int row0, rstep, nrows;
 };
 
+// numpy product (c + 0i) * a
+__device__ __forceinline__ double2 scale_np(double c, double2 a) {
+  return cmul_np(make_double2(c, 0.0), a);
+}
+
+struct Slots {
+  double2 s0, s1, s2, s3;   // amplitudes in reference slot order
+  int pD, pL, pR, pU;       // slot of each direction
+};
+
+// reference slot order of vertex (x, gy) on an nx x ny torus
+__device__ __forceinline__ Slots order_slots(int x, int gy, int nx, int ny, double2 vD, double2 vL,
+                                             double2 vR, double2 vU) {
+  Slots o;
+  const bool xe = (x == 0) | (x == nx - 1);
+  const double2 h0 = xe ? vR : vL;
+  const double2 h1 = xe ? vL : vR;
+  int ph0, ph1;
+  if (gy == 0) {
+    o.s0 = h0; o.s1 = h1; o.s2 = vU; o.s3 = vD;
+    ph0 = 0; ph1 = 1; o.pU = 2; o.pD = 3;
+  } else if (gy == ny - 1) {
+    o.s0 = vU; o.s1 = vD; o.s2 = h0; o.s3 = h1;
+    o.pU = 0; o.pD = 1; ph0 = 2; ph1 = 3;
+  } else {
+    o.s0 = vD; o.s1 = h0; o.s2 = h1; o.s3 = vU;
+    o.pD = 0; ph0 = 1; ph1 = 2; o.pU = 3;
+  }
+  o.pL = xe ? ph1 : ph0;
+  o.pR = xe ? ph0 : ph1;
+  return o;
+}
+
+__device__ __forceinline__ double2 pick(int p, double2 a0, double2 a1, double2 a2, double2 a3) {
+  double2 r = a0;
+  r = (p == 1) ? a1 : r;
+  r = (p == 2) ? a2 : r;
+  r = (p == 3) ? a3 : r;
+  return r;
+}
+
+// The four row values of U that vertex w feeds (one per direction e):
+// O_e = p0 + ((p1 + p2) + p3), p_i = (i == slot(e) ? -0.5 : 0.5) * s_i, numpy's
+// reduceat over the row; -psi_e for a marked vertex.
+__device__ __forceinline__ void vertex_outputs(const Slots& o, bool marked, double2 vD, double2 vL,
+                                               double2 vR, double2 vU, double2& oD, double2& oL,
+                                               double2& oR, double2& oU) {
+  if (marked) {
+    oD = scale_np(-1.0, vD);
+    oL = scale_np(-1.0, vL);
+    oR = scale_np(-1.0, vR);
+    oU = scale_np(-1.0, vU);
+    return;
+  }
+  const double2 q0 = scale_np(0.5, o.s0), q1 = scale_np(0.5, o.s1);
+  const double2 q2 = scale_np(0.5, o.s2), q3 = scale_np(0.5, o.s3);
+  const double2 n0 = scale_np(-0.5, o.s0), n1 = scale_np(-0.5, o.s1);
+  const double2 n2 = scale_np(-0.5, o.s2), n3 = scale_np(-0.5, o.s3);
+  const double2 t12 = cadd(q1, q2);
+  const double2 O0 = cadd(n0, cadd(t12, q3));
+  const double2 O1 = cadd(q0, cadd(cadd(n1, q2), q3));
+  const double2 O2 = cadd(q0, cadd(cadd(q1, n2), q3));
+  const double2 O3 = cadd(q0, cadd(t12, n3));
+  oD = pick(o.pD, O0, O1, O2, O3);
+  oL = pick(o.pL, O0, O1, O2, O3);
+  oR = pick(o.pR, O0, O1, O2, O3);
+  oU = pick(o.pU, O0, O1, O2, O3);
+}
+
 void lattice_launch(int shift, cudaStream_t s, const Geom& g, const Rows& r, const double2* in,
                     double2* out, const uint32_t* bits, double* prob, int prob_row0,
                     const TraceArgs& tr);
 int lattice_check_shift(qwb_ctx* ctx, int shift);
+// temporally blocked single-GPU torus steps (lattice_tb.cu)
+int lattice_tb_depth(int64_t nx, int64_t ny);
+int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny,
+                      const double2* in, double2* out, const uint32_t* bits);
 int lattice_slab_geom(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, Geom* g);
 // part: 0 = all owned rows, 1 = first and last owned rows, 2 = interior owned rows
 Rows slab_rows(int64_t ny_local, int part);
