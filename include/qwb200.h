@@ -142,12 +142,17 @@ int qwb_lattice_to_planes(qwb_ctx* ctx, int64_t nx, int64_t ny, const qwb_z* arc
 int qwb_lattice_from_planes(qwb_ctx* ctx, int64_t nx, int64_t ny, const qwb_z* planes, qwb_z* arcs,
                             void* stream);
 /* Run `steps` coined steps ping-ponging between a (input) and b.  On return
- * *final_in_b_host says where the result is.  If trace != NULL, trace[s*n_trace+j]
- * receives p(trace_vertices_host[j]) of the state BEFORE step s (s < steps),
- * fused into the step kernel (coined.probability_distribution semantics).  */
+ * *final_in_b_host says where the result is.  The marked set is passed both as
+ * the device bitmap and as the sorted host list (marked_host[n_marked]); with
+ * <= 8 marked vertices and no trace, several steps are fused per HBM pass
+ * (temporally blocked wavefront kernel, lattice_tb.cu).  If trace != NULL,
+ * trace[s*n_trace+j] receives p(trace_vertices_host[j]) of the state BEFORE
+ * step s (s < steps), fused into the step kernel
+ * (coined.probability_distribution semantics).                               */
 int qwb_lattice_run(qwb_ctx* ctx, int64_t nx, int64_t ny, int shift, const uint32_t* marked_bits,
-                    qwb_z* a, qwb_z* b, int64_t steps, const int64_t* trace_vertices_host,
-                    int n_trace, double* trace, int* final_in_b_host, void* stream);
+                    const int64_t* marked_host, int64_t n_marked, qwb_z* a, qwb_z* b, int64_t steps,
+                    const int64_t* trace_vertices_host, int n_trace, double* trace,
+                    int* final_in_b_host, void* stream);
 /* One step with an optional fused full distribution p of the INPUT state.    */
 int qwb_lattice_step(qwb_ctx* ctx, int64_t nx, int64_t ny, int shift, const uint32_t* marked_bits,
                      const qwb_z* in, qwb_z* out, double* prob_in, void* stream);

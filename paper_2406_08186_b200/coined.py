@@ -214,6 +214,8 @@ class _LatticeRunner:
         self.shift = N.SHIFT[spec.shift]
         self.bits = None
         marked = spec.active_marked
+        self.marked = tuple(marked)
+        self.marked_arr = N.i64_array(marked)
         if marked:
             self.bits = torch.empty((self.n + 31) // 32, dtype=torch.int32, device=engine.torch_device)
             mk = _marked_tensor(engine, marked)
@@ -231,9 +233,9 @@ class _LatticeRunner:
             return
         flag = C.c_int(0)
         tv = N.i64_array(trace_vertices)
-        self.engine.call("qwb_lattice_run", self.nx, self.ny, self.shift, N.ptr(self.bits), N.ptr(self.a),
-                         N.ptr(self.b), int(steps), tv, len(trace_vertices), N.ptr(trace),
-                         C.byref(flag), self.engine.stream())
+        self.engine.call("qwb_lattice_run", self.nx, self.ny, self.shift, N.ptr(self.bits),
+                         self.marked_arr, len(self.marked), N.ptr(self.a), N.ptr(self.b), int(steps), tv,
+                         len(trace_vertices), N.ptr(trace), C.byref(flag), self.engine.stream())
         if flag.value:
             self.a, self.b = self.b, self.a
 

@@ -320,8 +320,9 @@ int qwb_lattice_step(qwb_ctx* ctx, int64_t nx, int64_t ny, int shift, const uint
 }
 
 int qwb_lattice_run(qwb_ctx* ctx, int64_t nx, int64_t ny, int shift, const uint32_t* marked_bits,
-                    qwb_z* a, qwb_z* b, int64_t steps, const int64_t* trace_vertices_host,
-                    int n_trace, double* trace, int* final_in_b_host, void* stream) {
+                    const int64_t* marked_host, int64_t n_marked, qwb_z* a, qwb_z* b, int64_t steps,
+                    const int64_t* trace_vertices_host, int n_trace, double* trace,
+                    int* final_in_b_host, void* stream) {
   QWB_BEGIN(ctx);
   int st = check_dims(ctx, nx, ny);
   if (!st) st = qwb::lattice_check_shift(ctx, shift);
@@ -344,10 +345,13 @@ int qwb_lattice_run(qwb_ctx* ctx, int64_t nx, int64_t ny, int shift, const uint3
   int swaps = 0;
   int64_t k = 0;
   // T coined steps per HBM pass when no per-step trace is requested
-  const int depth = trace ? 0 : qwb::lattice_tb_depth(nx, ny);
+  if (n_marked > 0 && (!marked_bits || !marked_host))
+    QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "marked vertices need both the bitmap and the host list");
+  const int depth = trace ? 0 : qwb::lattice_tb_depth(nx, ny, n_marked);
   if (depth > 0) {
     for (; k + depth <= steps; k += depth) {
-      st = qwb::lattice_tb_launch(ctx, depth, shift, s, (int)nx, (int)ny, cur, nxt, marked_bits);
+      st = qwb::lattice_tb_launch(ctx, depth, shift, s, (int)nx, (int)ny, cur, nxt, marked_bits,
+                                  marked_host, n_marked);
       if (st) return st;
       double2* t = cur;
       cur = nxt;

@@ -1,33 +1,29 @@
 // lattice_tb.cu — temporally blocked torus walk: T coined steps per HBM pass.
 //
 // The single-step kernel (lattice.cu) already moves exactly the 32 B per arc
-// per step that one application of U needs, and runs at ~96 % of the measured
-// HBM copy bandwidth.  The only way past that roofline is to apply U several
-// times per trip through HBM.  Each CTA owns a 32 x 32 region of vertices, one
-// per thread, with the 4 direction amplitudes in registers:
+// per step that one application of U needs, at ~96 % of the measured HBM copy
+// bandwidth.  The only way past that roofline is to apply U several times per
+// trip through HBM.  Each CTA owns a region of 32 x (BY*V) vertices; a thread
+// owns V vertically adjacent vertices with their 4 direction amplitudes in
+// registers:
 //
-//   * the region's state arrives by cp.async into shared memory (prefetched
-//     one tile ahead, so HBM reads overlap the arithmetic of the current tile);
-//   * T steps run on chip.  A step is the same per-vertex formula as the
-//     single-step kernel (qwb::vertex_outputs — identical arithmetic, so the
-//     result stays bitwise equal to the reference); the pushes to x +- 1 go
-//     through warp shuffles (a warp is one region row), the pushes to y +- 1
-//     through a double-buffered shared-memory exchange (one barrier per step);
+//   * the region's state arrives by cp.async into shared memory, prefetched one
+//     tile ahead, so HBM reads overlap the arithmetic of the current tile;
+//   * T steps run on chip.  A step is the per-vertex formula of the single-step
+//     kernel (identical arithmetic => still bitwise equal to the reference).
+//     Pushes to x +- 1 go through warp shuffles (a warp is one region row of 32
+//     columns), pushes between a thread's own V rows stay in registers, and only
+//     the pushes across thread rows go through a double-buffered shared-memory
+//     exchange (one barrier per step);
 //   * values near the region edge go stale one ring per step, so after T steps
-//     the inner (32 - 2T)^2 vertices are exact and are written back.
+//     the inner (32 - 2T) x (BY*V - 2T) vertices are exact and are written.
 //
-// HBM traffic per T steps: 64 B x 32^2 read + 64 B x (32-2T)^2 written per
-// tile, i.e. for T = 4 about 11 B per arc-step instead of 32.  Regions wrap
-// around the torus (modular global coordinates), so any nx, ny >= 3 works.
+// Regions wrap around the torus (modular global coordinates): any nx, ny >= 3.
+#include <string.h>
+
 #include "qwb_lattice.cuh"
 
 namespace {
-
-using qwb::order_slots;
-using qwb::Slots;
-
-constexpr int R = 32;          // region side; blockDim = (32, 32)
-constexpr int RR = R * R;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -36,7 +32,7 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-__device__ __forceinline__ int wrap(int v, int n) {
+__device__ __forceinline__ int wrapc(int v, int n) {
   v = v < 0 ? v + n : v;
   return v >= n ? v - n : v;
 }
@@ -48,137 +44,347 @@ __device__ __forceinline__ double2 shfl_up2(double2 v) {
   return make_double2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
 }
 
-template <int SHIFT, bool MARKED, int T>
-__global__ void __launch_bounds__(RR, 1)
+template <int BY, int V>
+struct TbShape {
+  static constexpr int RX = 32;            // region columns (= warp lanes)
+  static constexpr int RY = BY * V;        // region rows
+  static constexpr int NT = 32 * BY;       // threads
+  static constexpr int REG = RX * RY;      // region vertices
+  static constexpr size_t smem_bytes() { return (4 * (size_t)REG + 4 * (size_t)NT) * sizeof(double2); }
+};
+
+template <int SHIFT, bool MARKED, int T, int BY, int V>
+__global__ void __launch_bounds__(32 * BY, 1)
 lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __restrict__ out,
                   const uint32_t* __restrict__ bits, int tiles_x, int ntiles) {
-  constexpr int O = R - 2 * T;   // owned (exact) side
+  using S = TbShape<BY, V>;
+  constexpr int OX = S::RX - 2 * T, OY = S::RY - 2 * T;   // exact (owned) block
   extern __shared__ double2 sm[];
-  double2* stage = sm;            // [4][R][R] next tile's amplitudes
-  double2* xD = sm + 4 * RR;      // [2][R][R] O_D exchange
-  double2* xU = xD + 2 * RR;      // [2][R][R] O_U exchange
+  double2* stage = sm;                 // [4][RY][RX] next tile's amplitudes
+  double2* xD = sm + 4 * S::REG;       // [2][BY][32] O_D of each thread's lowest row
+  double2* xU = xD + 2 * S::NT;        // [2][BY][32] O_U of each thread's highest row
   const int tx = threadIdx.x, ty = threadIdx.y;
-  const int me = ty * R + tx;
+  const int tid = ty * 32 + tx;
   const int64_t n = (int64_t)nx * ny;
+
+  auto prefetch = [&](int tile) {
+    const int bx = (tile % tiles_x) * OX - T + tx;
+    const int by = (tile / tiles_x) * OY - T + ty * V;
+    const int gx = wrapc(bx, nx);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int gy = wrapc(by + j, ny);
+      const int64_t w = (int64_t)gy * nx + gx;
+      const int li = (ty * V + j) * 32 + tx;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) cp_async16(stage + p * S::REG + li, in + p * n + w);
+    }
+  };
 
   int tile = blockIdx.x;
   if (tile >= ntiles) return;
-  {
-    const int gx = wrap((tile % tiles_x) * O - T + tx, nx);
-    const int gy = wrap((tile / tiles_x) * O - T + ty, ny);
-    const int64_t w = (int64_t)gy * nx + gx;
-#pragma unroll
-    for (int p = 0; p < 4; ++p) cp_async16(stage + p * RR + me, in + p * n + w);
-    cp_commit();
-  }
+  prefetch(tile);
+  cp_commit();
   for (; tile < ntiles; tile += gridDim.x) {
-    const int x0 = (tile % tiles_x) * O, y0 = (tile / tiles_x) * O;
-    const int gx = wrap(x0 - T + tx, nx);
-    const int gy = wrap(y0 - T + ty, ny);
+    const int x0 = (tile % tiles_x) * OX, y0 = (tile / tiles_x) * OY;
+    const int gx = wrapc(x0 - T + tx, nx);
+    int gy[V];
+    double2 vD[V], vL[V], vR[V], vU[V];
     cp_wait_all();
     __syncthreads();
-    double2 vD = stage[me], vL = stage[RR + me], vR = stage[2 * RR + me], vU = stage[3 * RR + me];
-    __syncthreads();
-    const int nt = tile + gridDim.x;
-    if (nt < ntiles) {
-      const int ngx = wrap((nt % tiles_x) * O - T + tx, nx);
-      const int ngy = wrap((nt / tiles_x) * O - T + ty, ny);
-      const int64_t nw = (int64_t)ngy * nx + ngx;
 #pragma unroll
-      for (int p = 0; p < 4; ++p) cp_async16(stage + p * RR + me, in + p * n + nw);
+    for (int j = 0; j < V; ++j) {
+      gy[j] = wrapc(y0 - T + ty * V + j, ny);
+      const int li = (ty * V + j) * 32 + tx;
+      vD[j] = stage[li];
+      vL[j] = stage[S::REG + li];
+      vR[j] = stage[2 * S::REG + li];
+      vU[j] = stage[3 * S::REG + li];
     }
+    __syncthreads();
+    if (tile + (int)gridDim.x < ntiles) prefetch(tile + gridDim.x);
     cp_commit();
-    bool marked = false;
-    if (MARKED) {
-      const int64_t wg = (int64_t)gy * nx + gx;
-      marked = (__ldg(bits + (wg >> 5)) >> (wg & 31)) & 1u;
+    bool mk[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      mk[j] = false;
+      if (MARKED) {
+        const int64_t wg = (int64_t)gy[j] * nx + gx;
+        mk[j] = (__ldg(bits + (wg >> 5)) >> (wg & 31)) & 1u;
+      }
     }
 #pragma unroll
     for (int t = 0; t < T; ++t) {
-      const Slots o = order_slots(gx, gy, nx, ny, vD, vL, vR, vU);
-      double2 oD, oL, oR, oU;
-      qwb::vertex_outputs(o, marked, vD, vL, vR, vU, oD, oL, oR, oU);
-      const int b = (t & 1) * RR;
-      xD[b + me] = oD;
-      xU[b + me] = oU;
-      const double2 fromRight = shfl_down2(oL);   // O_L of (x+1, y)
-      const double2 fromLeft = shfl_up2(oR);      // O_R of (x-1, y)
+      double2 oD[V], oL[V], oR[V], oU[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j)
+        qwb::vertex_outputs_fin(gx, gy[j], nx, ny, mk[j], vD[j], vL[j], vR[j], vU[j], oD[j], oL[j],
+                                oR[j], oU[j]);
+      const int b = (t & 1) * S::NT;
+      xD[b + tid] = oD[0];
+      xU[b + tid] = oU[V - 1];
+      double2 fromRight[V], fromLeft[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        fromRight[j] = shfl_down2(oL[j]);   // O_L of (x+1, y)
+        fromLeft[j] = shfl_up2(oR[j]);      // O_R of (x-1, y)
+      }
       __syncthreads();
-      const double2 fromAbove = (ty < R - 1) ? xD[b + me + R] : oD;   // O_D of (x, y+1)
-      const double2 fromBelow = (ty > 0) ? xU[b + me - R] : oU;       // O_U of (x, y-1)
-      if (SHIFT == QWB_SHIFT_FLIPFLOP) {
-        vU = fromAbove; vD = fromBelow; vR = fromRight; vL = fromLeft;
-      } else {
-        vD = fromAbove; vU = fromBelow; vL = fromRight; vR = fromLeft;
+      double2 fromAbove[V], fromBelow[V];   // O_D of (x, y+1), O_U of (x, y-1)
+#pragma unroll
+      for (int j = 0; j < V - 1; ++j) fromAbove[j] = oD[j + 1];
+      fromAbove[V - 1] = (ty < BY - 1) ? xD[b + tid + 32] : oD[V - 1];
+#pragma unroll
+      for (int j = 1; j < V; ++j) fromBelow[j] = oU[j - 1];
+      fromBelow[0] = (ty > 0) ? xU[b + tid - 32] : oU[0];
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        if (SHIFT == QWB_SHIFT_FLIPFLOP) {
+          vU[j] = fromAbove[j]; vD[j] = fromBelow[j]; vR[j] = fromRight[j]; vL[j] = fromLeft[j];
+        } else {
+          vD[j] = fromAbove[j]; vU[j] = fromBelow[j]; vL[j] = fromRight[j]; vR[j] = fromLeft[j];
+        }
       }
     }
-    if (tx >= T && tx < T + O && ty >= T && ty < T + O && x0 + tx - T < nx && y0 + ty - T < ny) {
-      const int64_t w = (int64_t)gy * nx + gx;
-      __stcs(out + w, vD);
-      __stcs(out + n + w, vL);
-      __stcs(out + 2 * n + w, vR);
-      __stcs(out + 3 * n + w, vU);
+    const bool col_ok = tx >= T && tx < T + OX && x0 + tx - T < nx;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int ly = ty * V + j;
+      if (col_ok && ly >= T && ly < T + OY && y0 + ly - T < ny) {
+        const int64_t w = (int64_t)gy[j] * nx + gx;
+        __stcs(out + w, vD[j]);
+        __stcs(out + n + w, vL[j]);
+        __stcs(out + 2 * n + w, vR[j]);
+        __stcs(out + 3 * n + w, vU[j]);
+      }
     }
   }
   cp_wait_all();
 }
 
-template <int SHIFT, bool MARKED, int T>
+template <int SHIFT, bool MARKED, int T, int BY, int V>
 int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const double2* in, double2* out,
                 const uint32_t* bits) {
-  constexpr int O = R - 2 * T;
-  const int tiles_x = (nx + O - 1) / O, tiles_y = (ny + O - 1) / O;
+  using Sh = TbShape<BY, V>;
+  constexpr int OX = Sh::RX - 2 * T, OY = Sh::RY - 2 * T;
+  const int tiles_x = (nx + OX - 1) / OX, tiles_y = (ny + OY - 1) / OY;
   const int ntiles = tiles_x * tiles_y;
-  const size_t smem = (4 + 4) * RR * sizeof(double2);
+  const size_t smem = Sh::smem_bytes();
   static bool configured[256] = {};   // per instantiation and device
   const int dev = ctx->device & 255;
   if (!configured[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(lattice_tb_kernel<SHIFT, MARKED, T>,
+    cudaError_t e = cudaFuncSetAttribute(lattice_tb_kernel<SHIFT, MARKED, T, BY, V>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return qwb::cuda_status(ctx, e, "cudaFuncSetAttribute(lattice_tb)");
     configured[dev] = true;
   }
   const int grid = ntiles < ctx->num_sms ? ntiles : ctx->num_sms;
-  lattice_tb_kernel<SHIFT, MARKED, T><<<grid, dim3(R, R), smem, s>>>(nx, ny, in, out, bits, tiles_x, ntiles);
+  lattice_tb_kernel<SHIFT, MARKED, T, BY, V><<<grid, dim3(32, BY), smem, s>>>(nx, ny, in, out, bits,
+                                                                               tiles_x, ntiles);
+  return QWB_OK;
+}
+
+template <int T, int BY, int V>
+int launch_tb(qwb_ctx* ctx, int shift, cudaStream_t s, int nx, int ny, const double2* in,
+              double2* out, const uint32_t* bits) {
+  if (shift == QWB_SHIFT_FLIPFLOP) {
+    return bits ? launch_tb_t<QWB_SHIFT_FLIPFLOP, true, T, BY, V>(ctx, s, nx, ny, in, out, bits)
+                : launch_tb_t<QWB_SHIFT_FLIPFLOP, false, T, BY, V>(ctx, s, nx, ny, in, out, bits);
+  }
+  return bits ? launch_tb_t<QWB_SHIFT_PERSISTENT, true, T, BY, V>(ctx, s, nx, ny, in, out, bits)
+              : launch_tb_t<QWB_SHIFT_PERSISTENT, false, T, BY, V>(ctx, s, nx, ny, in, out, bits);
+}
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
+
+// ---------------------------------------------------------------------------
+// Wavefront variant: one warp = one column strip of 32 lanes that streams
+// along y.  Level t+1 of row r needs level t of rows r-1, r, r+1 only, so a
+// warp keeps, for each level, the outputs of the last two rows in registers
+// and completes one row per level per iteration (a skewed wavefront): no
+// shared memory, no barriers, warps fully independent.  Pushes along x use
+// shuffles; pushes along y are register moves.  Redundant work: 2T halo lanes
+// of 32 and 2T warm-up rows per strip.
+// ---------------------------------------------------------------------------
+struct MarkedList {
+  int n;
+  int64_t v[8];
+};
+
+__device__ __forceinline__ bool in_list(const MarkedList& m, int64_t w) {
+  bool r = false;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r |= (k < m.n) && (m.v[k] == w);
+  return r;
+}
+
+__device__ __forceinline__ void ld4(const double2* __restrict__ in, int64_t n, int64_t w, double2& d,
+                                    double2& l, double2& r, double2& u) {
+  d = __ldcs(in + w);
+  l = __ldcs(in + n + w);
+  r = __ldcs(in + 2 * n + w);
+  u = __ldcs(in + 3 * n + w);
+}
+
+template <int SHIFT, bool MARKED, int T>
+__global__ void __launch_bounds__(128)
+lattice_wf_kernel(int nx, int ny, const double2* __restrict__ in, double2* __restrict__ out,
+                  MarkedList mk, int strips_x, int nstrips, int L) {
+  constexpr int OX = 32 - 2 * T;
+  const int lane = threadIdx.x & 31;
+  const int strip = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+  if (strip >= nstrips) return;
+  const int x0 = (strip % strips_x) * OX, y0 = (strip / strips_x) * L;
+  const int yend = min(y0 + L, ny);
+  const int gx = wrapc(x0 - T + lane, nx);
+  const bool col_out = lane >= T && lane < T + OX && x0 + lane - T < nx;
+  const int64_t n = (int64_t)nx * ny;
+  const int ys = y0 - T;
+  const int rows = (yend - y0) + 2 * T;
+
+  // per level t-1 (0..T-1): outputs of the previous row (L, R, U needed) and
+  // the U output of the row before it
+  double2 pOL[T], pOR[T], pOU[T], ppOU[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    pOL[t] = pOR[t] = pOU[t] = ppOU[t] = make_double2(0.0, 0.0);
+  }
+  double2 nD, nL, nR, nU;
+  ld4(in, n, (int64_t)wrapc(ys, ny) * nx + gx, nD, nL, nR, nU);
+  for (int i = 0; i < rows; ++i) {
+    double2 sD = nD, sL = nL, sR = nR, sU = nU;
+    if (i + 1 < rows) ld4(in, n, (int64_t)wrapc(ys + i + 1, ny) * nx + gx, nD, nL, nR, nU);
+    const int r = ys + i;
+    int gy = wrapc(r, ny);
+    double2 cD, cL, cR, cU;
+    {
+      const bool m = MARKED && in_list(mk, (int64_t)gy * nx + gx);
+      qwb::vertex_outputs_fin(gx, gy, nx, ny, m, sD, sL, sR, sU, cD, cL, cR, cU);
+    }
+#pragma unroll
+    for (int t = 1; t <= T; ++t) {
+      const double2 fromAbove = cD;                    // O_D of row r-t+1
+      const double2 fromRight = shfl_down2(pOL[t - 1]);   // O_L of (x+1, r-t)
+      const double2 fromLeft = shfl_up2(pOR[t - 1]);      // O_R of (x-1, r-t)
+      const double2 fromBelow = ppOU[t - 1];           // O_U of row r-t-1
+      ppOU[t - 1] = pOU[t - 1];
+      pOL[t - 1] = cL;
+      pOR[t - 1] = cR;
+      pOU[t - 1] = cU;
+      if (SHIFT == QWB_SHIFT_FLIPFLOP) {
+        sU = fromAbove; sD = fromBelow; sR = fromRight; sL = fromLeft;
+      } else {
+        sD = fromAbove; sU = fromBelow; sL = fromRight; sR = fromLeft;
+      }
+      gy = gy == 0 ? ny - 1 : gy - 1;                  // row r - t
+      if (t < T) {
+        const bool m = MARKED && in_list(mk, (int64_t)gy * nx + gx);
+        qwb::vertex_outputs_fin(gx, gy, nx, ny, m, sD, sL, sR, sU, cD, cL, cR, cU);
+      } else if (i >= 2 * T && col_out) {
+        const int64_t w = (int64_t)gy * nx + gx;
+        __stcs(out + w, sD);
+        __stcs(out + n + w, sL);
+        __stcs(out + 2 * n + w, sR);
+        __stcs(out + 3 * n + w, sU);
+      }
+    }
+  }
+}
+
+template <int SHIFT, bool MARKED, int T>
+int launch_wf_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const double2* in, double2* out,
+                const MarkedList& mk) {
+  constexpr int OX = 32 - 2 * T;
+  const int strips_x = (nx + OX - 1) / OX;
+  // strip length: long strips amortise the 2T warm-up rows, but keep >= ~16
+  // warps per SM in flight
+  int L = env_int("QWB_LATTICE_L", 0);
+  if (L <= 0) {
+    const long long want = (long long)ctx->num_sms * 16;
+    L = 256;
+    while (L > 32 && (long long)strips_x * ((ny + L - 1) / L) < want) L /= 2;
+  }
+  const int strips_y = (ny + L - 1) / L;
+  const int nstrips = strips_x * strips_y;
+  const int threads = 128;
+  const int blocks = (nstrips * 32 + threads - 1) / threads;
+  lattice_wf_kernel<SHIFT, MARKED, T><<<blocks, threads, 0, s>>>(nx, ny, in, out, mk, strips_x, nstrips, L);
   return QWB_OK;
 }
 
 template <int T>
-int launch_tb(qwb_ctx* ctx, int shift, cudaStream_t s, int nx, int ny, const double2* in, double2* out,
-              const uint32_t* bits) {
-  if (shift == QWB_SHIFT_FLIPFLOP) {
-    return bits ? launch_tb_t<QWB_SHIFT_FLIPFLOP, true, T>(ctx, s, nx, ny, in, out, bits)
-                : launch_tb_t<QWB_SHIFT_FLIPFLOP, false, T>(ctx, s, nx, ny, in, out, bits);
-  }
-  return bits ? launch_tb_t<QWB_SHIFT_PERSISTENT, true, T>(ctx, s, nx, ny, in, out, bits)
-              : launch_tb_t<QWB_SHIFT_PERSISTENT, false, T>(ctx, s, nx, ny, in, out, bits);
+int launch_wf(qwb_ctx* ctx, int shift, cudaStream_t s, int nx, int ny, const double2* in,
+              double2* out, const MarkedList& mk) {
+  const bool m = mk.n > 0;
+  if (shift == QWB_SHIFT_FLIPFLOP)
+    return m ? launch_wf_t<QWB_SHIFT_FLIPFLOP, true, T>(ctx, s, nx, ny, in, out, mk)
+             : launch_wf_t<QWB_SHIFT_FLIPFLOP, false, T>(ctx, s, nx, ny, in, out, mk);
+  return m ? launch_wf_t<QWB_SHIFT_PERSISTENT, true, T>(ctx, s, nx, ny, in, out, mk)
+           : launch_wf_t<QWB_SHIFT_PERSISTENT, false, T>(ctx, s, nx, ny, in, out, mk);
 }
 
 }  // namespace
 
 namespace qwb {
 
-// steps per temporally blocked launch (0 = not available); 2, 4, 6 or 8
-int lattice_tb_depth(int64_t nx, int64_t ny) {
+// Steps per temporally blocked launch (0 = single-step kernel only).
+// QWB_LATTICE_T overrides (0, 2..8); QWB_LATTICE_KIND picks the wavefront
+// ("wf", default) or the CTA-tile ("tile") variant; QWB_LATTICE_SHAPE the tile shape.
+int lattice_tb_depth(int64_t nx, int64_t ny, int64_t n_marked) {
   static int depth = -1;
   if (depth < 0) {
-    const char* e = getenv("QWB_LATTICE_T");
-    depth = e ? atoi(e) : 4;
-    if (depth != 0 && depth != 2 && depth != 4 && depth != 6 && depth != 8) depth = 4;
+    depth = env_int("QWB_LATTICE_T", 6);
+    if (depth < 0 || depth > 8 || depth == 1) depth = 6;
   }
   if (nx < 64 || ny < 64) return 0;   // tiny lattices: the single-step kernel is launch-bound anyway
+  if (n_marked > 8) return 0;         // the fused kernels take the marked set as a short list
   return depth;
 }
 
 int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny,
-                      const double2* in, double2* out, const uint32_t* bits) {
-  switch (depth) {
-    case 2: return launch_tb<2>(ctx, shift, s, nx, ny, in, out, bits);
-    case 4: return launch_tb<4>(ctx, shift, s, nx, ny, in, out, bits);
-    case 6: return launch_tb<6>(ctx, shift, s, nx, ny, in, out, bits);
-    case 8: return launch_tb<8>(ctx, shift, s, nx, ny, in, out, bits);
-    default: QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "unsupported temporal block depth %d", depth);
+                      const double2* in, double2* out, const uint32_t* bits,
+                      const int64_t* marked_host, int64_t n_marked) {
+  static int kind = -1;
+  if (kind < 0) {
+    const char* e = getenv("QWB_LATTICE_KIND");
+    kind = (e && strcmp(e, "tile") == 0) ? 1 : 0;
   }
+  if (kind == 0) {
+    MarkedList mk{};
+    mk.n = (int)n_marked;
+    for (int k = 0; k < mk.n; ++k) mk.v[k] = marked_host[k];
+    switch (depth) {
+      case 2: return launch_wf<2>(ctx, shift, s, nx, ny, in, out, mk);
+      case 3: return launch_wf<3>(ctx, shift, s, nx, ny, in, out, mk);
+      case 4: return launch_wf<4>(ctx, shift, s, nx, ny, in, out, mk);
+      case 5: return launch_wf<5>(ctx, shift, s, nx, ny, in, out, mk);
+      case 6: return launch_wf<6>(ctx, shift, s, nx, ny, in, out, mk);
+      case 7: return launch_wf<7>(ctx, shift, s, nx, ny, in, out, mk);
+      case 8: return launch_wf<8>(ctx, shift, s, nx, ny, in, out, mk);
+      default: QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "unsupported temporal block depth %d", depth);
+    }
+  }
+  static int shape = -1;
+  if (shape < 0) shape = env_int("QWB_LATTICE_SHAPE", 2);
+  if (depth > 4) depth = 4;
+  // shape 0: 32x32 threads, 1 vertex each; 1: 32x16 threads, 2 rows each (32x32 region);
+  // 2: 32x24 threads, 2 rows each (32x48 region)
+#define QWB_TB_CASE(T_)                                                                     \
+  case T_:                                                                                  \
+    if (shape == 0) return launch_tb<T_, 32, 1>(ctx, shift, s, nx, ny, in, out, bits);      \
+    if (shape == 2) return launch_tb<T_, 24, 2>(ctx, shift, s, nx, ny, in, out, bits);      \
+    return launch_tb<T_, 16, 2>(ctx, shift, s, nx, ny, in, out, bits);
+  switch (depth) {
+    QWB_TB_CASE(2)
+    QWB_TB_CASE(3)
+    QWB_TB_CASE(4)
+    default:
+      QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "unsupported temporal block depth %d", depth);
+  }
+#undef QWB_TB_CASE
 }
 
 }  // namespace qwb

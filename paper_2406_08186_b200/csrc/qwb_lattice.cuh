@@ -95,14 +95,73 @@ __device__ __forceinline__ void vertex_outputs(const Slots& o, bool marked, doub
   oU = pick(o.pU, O0, O1, O2, O3);
 }
 
+// ---- finite-input fast forms (used by the temporally blocked kernel) --------
+// numpy's (c + 0i) * s is (fma(c, s.x, -(0*s.y)), fma(c, s.y, 0*s.x)).  For
+// finite s, 0*v is the signed zero copysign(0, v): computing it with integer
+// bit operations keeps the result bitwise identical (zero signs included) at
+// one FP64 op per component instead of two.  States are finite by
+// construction (move_to_device rejects NaN/Inf; U is unitary).
+__device__ __forceinline__ double zsign(double v) {   // 0 * v for finite v
+  return __longlong_as_double(__double_as_longlong(v) & (long long)0x8000000000000000ULL);
+}
+__device__ __forceinline__ double nzsign(double v) {  // -(0 * v) for finite v
+  return __longlong_as_double((__double_as_longlong(v) & (long long)0x8000000000000000ULL) ^
+                              (long long)0x8000000000000000ULL);
+}
+__device__ __forceinline__ double2 scale_fin(double c, double2 s) {
+  return make_double2(__fma_rn(c, s.x, nzsign(s.y)), __fma_rn(c, s.y, zsign(s.x)));
+}
+
+// vertex_outputs for finite inputs; interior vertices (slot order D L R U)
+// skip the slot permutation entirely.
+__device__ __forceinline__ void vertex_outputs_fin(int gx, int gy, int nx, int ny, bool marked,
+                                                   double2 vD, double2 vL, double2 vR, double2 vU,
+                                                   double2& oD, double2& oL, double2& oR, double2& oU) {
+  if (marked) {
+    oD = scale_fin(-1.0, vD);
+    oL = scale_fin(-1.0, vL);
+    oR = scale_fin(-1.0, vR);
+    oU = scale_fin(-1.0, vU);
+    return;
+  }
+  const bool interior = (gx > 0) & (gx < nx - 1) & (gy > 0) & (gy < ny - 1);
+  if (interior) {
+    const double2 qD = scale_fin(0.5, vD), qL = scale_fin(0.5, vL);
+    const double2 qR = scale_fin(0.5, vR), qU = scale_fin(0.5, vU);
+    const double2 nD = scale_fin(-0.5, vD), nL = scale_fin(-0.5, vL);
+    const double2 nR = scale_fin(-0.5, vR), nU = scale_fin(-0.5, vU);
+    const double2 t = cadd(qL, qR);
+    oD = cadd(nD, cadd(t, qU));
+    oL = cadd(qD, cadd(cadd(nL, qR), qU));
+    oR = cadd(qD, cadd(cadd(qL, nR), qU));
+    oU = cadd(qD, cadd(t, nU));
+    return;
+  }
+  const Slots o = order_slots(gx, gy, nx, ny, vD, vL, vR, vU);
+  const double2 q0 = scale_fin(0.5, o.s0), q1 = scale_fin(0.5, o.s1);
+  const double2 q2 = scale_fin(0.5, o.s2), q3 = scale_fin(0.5, o.s3);
+  const double2 n0 = scale_fin(-0.5, o.s0), n1 = scale_fin(-0.5, o.s1);
+  const double2 n2 = scale_fin(-0.5, o.s2), n3 = scale_fin(-0.5, o.s3);
+  const double2 t12 = cadd(q1, q2);
+  const double2 O0 = cadd(n0, cadd(t12, q3));
+  const double2 O1 = cadd(q0, cadd(cadd(n1, q2), q3));
+  const double2 O2 = cadd(q0, cadd(cadd(q1, n2), q3));
+  const double2 O3 = cadd(q0, cadd(t12, n3));
+  oD = pick(o.pD, O0, O1, O2, O3);
+  oL = pick(o.pL, O0, O1, O2, O3);
+  oR = pick(o.pR, O0, O1, O2, O3);
+  oU = pick(o.pU, O0, O1, O2, O3);
+}
+
 void lattice_launch(int shift, cudaStream_t s, const Geom& g, const Rows& r, const double2* in,
                     double2* out, const uint32_t* bits, double* prob, int prob_row0,
                     const TraceArgs& tr);
 int lattice_check_shift(qwb_ctx* ctx, int shift);
 // temporally blocked single-GPU torus steps (lattice_tb.cu)
-int lattice_tb_depth(int64_t nx, int64_t ny);
+int lattice_tb_depth(int64_t nx, int64_t ny, int64_t n_marked);
 int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny,
-                      const double2* in, double2* out, const uint32_t* bits);
+                      const double2* in, double2* out, const uint32_t* bits,
+                      const int64_t* marked_host, int64_t n_marked);
 int lattice_slab_geom(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, Geom* g);
 // part: 0 = all owned rows, 1 = first and last owned rows, 2 = interior owned rows
 Rows slab_rows(int64_t ny_local, int part);
