@@ -9,12 +9,14 @@
 //
 //   * the region's state arrives by cp.async into shared memory, prefetched one
 //     tile ahead, so HBM reads overlap the arithmetic of the current tile;
-//   * T steps run on chip.  A step is the per-vertex formula of the single-step
-//     kernel (identical arithmetic => still bitwise equal to the reference).
-//     Pushes to x +- 1 go through warp shuffles (a warp is one region row of 32
-//     columns), pushes between a thread's own V rows stay in registers, and only
-//     the pushes across thread rows go through a double-buffered shared-memory
-//     exchange (one barrier per step);
+//   * T steps run on chip, in doubled space (qwb_lattice.cuh "doubled-space
+//     forms": the operator 2U needs additions only — 20 FP64 adds per vertex
+//     and step — and the state is scaled by 2^-T on the way out, so the result
+//     has numpy's bits for every non-zero amplitude).  Pushes to x +- 1 go
+//     through warp shuffles (a warp is one region row of 32 columns), pushes
+//     between a thread's own V rows stay in registers, and only the pushes
+//     across thread rows go through a double-buffered shared-memory exchange
+//     (one barrier per step);
 //   * values near the region edge go stale one ring per step, so after T steps
 //     the inner (32 - 2T) x (BY*V - 2T) vertices are exact and are written.
 //
@@ -53,10 +55,70 @@ struct TbShape {
   static constexpr size_t smem_bytes() { return (4 * (size_t)REG + 4 * (size_t)NT) * sizeof(double2); }
 };
 
+// T steps of a tile on chip (see the file comment).  INTERIOR: every vertex of
+// the region is an unmarked interior vertex (no slot permutation, no branches).
+template <int SHIFT, bool MARKED, int T, int BY, int V, bool INTERIOR>
+__device__ __forceinline__ void tile_steps(int nx, int ny, int gx, const int (&gy)[V],
+                                           const uint32_t* __restrict__ bits, double2 (&vD)[V],
+                                           double2 (&vL)[V], double2 (&vR)[V], double2 (&vU)[V],
+                                           double2* xD, double2* xU, int tid, int ty) {
+  bool mk[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    mk[j] = false;
+    if (MARKED) {
+      const int64_t wg = (int64_t)gy[j] * nx + gx;
+      mk[j] = (__ldg(bits + (wg >> 5)) >> (wg & 31)) & 1u;
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    double2 oD[V], oL[V], oR[V], oU[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      if (INTERIOR)
+        qwb::vertex_outputs2_interior(vD[j], vL[j], vR[j], vU[j], oD[j], oL[j], oR[j], oU[j]);
+      else
+        qwb::vertex_outputs2(gx, gy[j], nx, ny, mk[j], vD[j], vL[j], vR[j], vU[j], oD[j], oL[j],
+                             oR[j], oU[j]);
+    }
+    const int b = (t & 1) * 32 * BY;
+    xD[b + tid] = oD[0];
+    xU[b + tid] = oU[V - 1];
+    double2 fromRight[V], fromLeft[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      fromRight[j] = shfl_down2(oL[j]);   // O_L of (x+1, y)
+      fromLeft[j] = shfl_up2(oR[j]);      // O_R of (x-1, y)
+    }
+    __syncthreads();
+    double2 fromAbove[V], fromBelow[V];   // O_D of (x, y+1), O_U of (x, y-1)
+#pragma unroll
+    for (int j = 0; j < V - 1; ++j) fromAbove[j] = oD[j + 1];
+    fromAbove[V - 1] = (ty < BY - 1) ? xD[b + tid + 32] : oD[V - 1];
+#pragma unroll
+    for (int j = 1; j < V; ++j) fromBelow[j] = oU[j - 1];
+    fromBelow[0] = (ty > 0) ? xU[b + tid - 32] : oU[0];
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      if (SHIFT == QWB_SHIFT_FLIPFLOP) {
+        vU[j] = fromAbove[j]; vD[j] = fromBelow[j]; vR[j] = fromRight[j]; vL[j] = fromLeft[j];
+      } else {
+        vD[j] = fromAbove[j]; vU[j] = fromBelow[j]; vL[j] = fromRight[j]; vR[j] = fromLeft[j];
+      }
+    }
+  }
+}
+
+struct MarkedList {   // up to 8 marked vertex ids; n < 0: more than 8 (use the bitmap)
+  int n;
+  int64_t v[8];
+};
+
 template <int SHIFT, bool MARKED, int T, int BY, int V>
 __global__ void __launch_bounds__(32 * BY, 1)
 lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __restrict__ out,
-                  const uint32_t* __restrict__ bits, int tiles_x, int ntiles) {
+                  const uint32_t* __restrict__ bits, MarkedList mk, int tiles_x, int ntiles) {
   using S = TbShape<BY, V>;
   constexpr int OX = S::RX - 2 * T, OY = S::RY - 2 * T;   // exact (owned) block
   extern __shared__ double2 sm[];
@@ -104,58 +166,35 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
     __syncthreads();
     if (tile + (int)gridDim.x < ntiles) prefetch(tile + gridDim.x);
     cp_commit();
-    bool mk[V];
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      mk[j] = false;
-      if (MARKED) {
-        const int64_t wg = (int64_t)gy[j] * nx + gx;
-        mk[j] = (__ldg(bits + (wg >> 5)) >> (wg & 31)) & 1u;
-      }
-    }
-#pragma unroll
-    for (int t = 0; t < T; ++t) {
-      double2 oD[V], oL[V], oR[V], oU[V];
-#pragma unroll
-      for (int j = 0; j < V; ++j)
-        qwb::vertex_outputs_fin(gx, gy[j], nx, ny, mk[j], vD[j], vL[j], vR[j], vU[j], oD[j], oL[j],
-                                oR[j], oU[j]);
-      const int b = (t & 1) * S::NT;
-      xD[b + tid] = oD[0];
-      xU[b + tid] = oU[V - 1];
-      double2 fromRight[V], fromLeft[V];
-#pragma unroll
-      for (int j = 0; j < V; ++j) {
-        fromRight[j] = shfl_down2(oL[j]);   // O_L of (x+1, y)
-        fromLeft[j] = shfl_up2(oR[j]);      // O_R of (x-1, y)
-      }
-      __syncthreads();
-      double2 fromAbove[V], fromBelow[V];   // O_D of (x, y+1), O_U of (x, y-1)
-#pragma unroll
-      for (int j = 0; j < V - 1; ++j) fromAbove[j] = oD[j + 1];
-      fromAbove[V - 1] = (ty < BY - 1) ? xD[b + tid + 32] : oD[V - 1];
-#pragma unroll
-      for (int j = 1; j < V; ++j) fromBelow[j] = oU[j - 1];
-      fromBelow[0] = (ty > 0) ? xU[b + tid - 32] : oU[0];
-#pragma unroll
-      for (int j = 0; j < V; ++j) {
-        if (SHIFT == QWB_SHIFT_FLIPFLOP) {
-          vU[j] = fromAbove[j]; vD[j] = fromBelow[j]; vR[j] = fromRight[j]; vL[j] = fromLeft[j];
-        } else {
-          vD[j] = fromAbove[j]; vU[j] = fromBelow[j]; vL[j] = fromRight[j]; vR[j] = fromLeft[j];
+    // regions that touch no torus edge and hold no marked vertex run a
+    // branch-free specialisation: every vertex is interior (slot order D L R U)
+    bool interior = x0 - T >= 1 && x0 - T + 31 <= nx - 2 && y0 - T >= 1 &&
+                    y0 - T + S::RY - 1 <= ny - 2;
+    if (MARKED && interior) {
+      if (mk.n < 0) {
+        interior = false;   // too many marked vertices for the list: general path
+      } else {
+        for (int k = 0; k < mk.n; ++k) {
+          const int mx = (int)(mk.v[k] % nx), my = (int)(mk.v[k] / nx);
+          interior &= !(mx >= x0 - T && mx < x0 - T + 32 && my >= y0 - T && my < y0 - T + S::RY);
         }
       }
     }
+    if (interior)
+      tile_steps<SHIFT, false, T, BY, V, true>(nx, ny, gx, gy, bits, vD, vL, vR, vU, xD, xU, tid, ty);
+    else
+      tile_steps<SHIFT, MARKED, T, BY, V, false>(nx, ny, gx, gy, bits, vD, vL, vR, vU, xD, xU, tid, ty);
     const bool col_ok = tx >= T && tx < T + OX && x0 + tx - T < nx;
+    constexpr double kScale = 1.0 / (double)(1 << T);   // undo the doubled-space steps (exact)
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       const int ly = ty * V + j;
       if (col_ok && ly >= T && ly < T + OY && y0 + ly - T < ny) {
         const int64_t w = (int64_t)gy[j] * nx + gx;
-        __stcs(out + w, vD[j]);
-        __stcs(out + n + w, vL[j]);
-        __stcs(out + 2 * n + w, vR[j]);
-        __stcs(out + 3 * n + w, vU[j]);
+        __stcs(out + w, make_double2(__dmul_rn(vD[j].x, kScale), __dmul_rn(vD[j].y, kScale)));
+        __stcs(out + n + w, make_double2(__dmul_rn(vL[j].x, kScale), __dmul_rn(vL[j].y, kScale)));
+        __stcs(out + 2 * n + w, make_double2(__dmul_rn(vR[j].x, kScale), __dmul_rn(vR[j].y, kScale)));
+        __stcs(out + 3 * n + w, make_double2(__dmul_rn(vU[j].x, kScale), __dmul_rn(vU[j].y, kScale)));
       }
     }
   }
@@ -164,7 +203,7 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
 
 template <int SHIFT, bool MARKED, int T, int BY, int V>
 int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const double2* in, double2* out,
-                const uint32_t* bits) {
+                const uint32_t* bits, const MarkedList& mk) {
   using Sh = TbShape<BY, V>;
   constexpr int OX = Sh::RX - 2 * T, OY = Sh::RY - 2 * T;
   const int tiles_x = (nx + OX - 1) / OX, tiles_y = (ny + OY - 1) / OY;
@@ -180,19 +219,19 @@ int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const double2* in,
   }
   const int grid = ntiles < ctx->num_sms ? ntiles : ctx->num_sms;
   lattice_tb_kernel<SHIFT, MARKED, T, BY, V><<<grid, dim3(32, BY), smem, s>>>(nx, ny, in, out, bits,
-                                                                               tiles_x, ntiles);
+                                                                               mk, tiles_x, ntiles);
   return QWB_OK;
 }
 
 template <int T, int BY, int V>
 int launch_tb(qwb_ctx* ctx, int shift, cudaStream_t s, int nx, int ny, const double2* in,
-              double2* out, const uint32_t* bits) {
+              double2* out, const uint32_t* bits, const MarkedList& mk) {
   if (shift == QWB_SHIFT_FLIPFLOP) {
-    return bits ? launch_tb_t<QWB_SHIFT_FLIPFLOP, true, T, BY, V>(ctx, s, nx, ny, in, out, bits)
-                : launch_tb_t<QWB_SHIFT_FLIPFLOP, false, T, BY, V>(ctx, s, nx, ny, in, out, bits);
+    return bits ? launch_tb_t<QWB_SHIFT_FLIPFLOP, true, T, BY, V>(ctx, s, nx, ny, in, out, bits, mk)
+                : launch_tb_t<QWB_SHIFT_FLIPFLOP, false, T, BY, V>(ctx, s, nx, ny, in, out, bits, mk);
   }
-  return bits ? launch_tb_t<QWB_SHIFT_PERSISTENT, true, T, BY, V>(ctx, s, nx, ny, in, out, bits)
-              : launch_tb_t<QWB_SHIFT_PERSISTENT, false, T, BY, V>(ctx, s, nx, ny, in, out, bits);
+  return bits ? launch_tb_t<QWB_SHIFT_PERSISTENT, true, T, BY, V>(ctx, s, nx, ny, in, out, bits, mk)
+              : launch_tb_t<QWB_SHIFT_PERSISTENT, false, T, BY, V>(ctx, s, nx, ny, in, out, bits, mk);
 }
 
 int env_int(const char* name, int dflt) {
@@ -209,11 +248,6 @@ int env_int(const char* name, int dflt) {
 // shuffles; pushes along y are register moves.  Redundant work: 2T halo lanes
 // of 32 and 2T warm-up rows per strip.
 // ---------------------------------------------------------------------------
-struct MarkedList {
-  int n;
-  int64_t v[8];
-};
-
 __device__ __forceinline__ bool in_list(const MarkedList& m, int64_t w) {
   bool r = false;
 #pragma unroll
@@ -254,18 +288,22 @@ lattice_wf_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
   }
   double2 nD, nL, nR, nU;
   ld4(in, n, (int64_t)wrapc(ys, ny) * nx + gx, nD, nL, nR, nU);
+#pragma unroll 1
   for (int i = 0; i < rows; ++i) {
     double2 sD = nD, sL = nL, sR = nR, sU = nU;
-    if (i + 1 < rows) ld4(in, n, (int64_t)wrapc(ys + i + 1, ny) * nx + gx, nD, nL, nR, nU);
+    {
+      const int nr = (i + 1 < rows) ? ys + i + 1 : ys + i;   // clamped prefetch, no branch
+      ld4(in, n, (int64_t)wrapc(nr, ny) * nx + gx, nD, nL, nR, nU);
+    }
     const int r = ys + i;
     int gy = wrapc(r, ny);
     double2 cD, cL, cR, cU;
     {
       const bool m = MARKED && in_list(mk, (int64_t)gy * nx + gx);
-      qwb::vertex_outputs_fin(gx, gy, nx, ny, m, sD, sL, sR, sU, cD, cL, cR, cU);
+      qwb::vertex_outputs2(gx, gy, nx, ny, m, sD, sL, sR, sU, cD, cL, cR, cU);
     }
 #pragma unroll
-    for (int t = 1; t <= T; ++t) {
+    for (int t = 1; t <= T; ++t) {   // level t holds 2^t psi_t (doubled-space steps)
       const double2 fromAbove = cD;                    // O_D of row r-t+1
       const double2 fromRight = shfl_down2(pOL[t - 1]);   // O_L of (x+1, r-t)
       const double2 fromLeft = shfl_up2(pOR[t - 1]);      // O_R of (x-1, r-t)
@@ -282,13 +320,14 @@ lattice_wf_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
       gy = gy == 0 ? ny - 1 : gy - 1;                  // row r - t
       if (t < T) {
         const bool m = MARKED && in_list(mk, (int64_t)gy * nx + gx);
-        qwb::vertex_outputs_fin(gx, gy, nx, ny, m, sD, sL, sR, sU, cD, cL, cR, cU);
+        qwb::vertex_outputs2(gx, gy, nx, ny, m, sD, sL, sR, sU, cD, cL, cR, cU);
       } else if (i >= 2 * T && col_out) {
+        constexpr double kScale = 1.0 / (double)(1 << T);
         const int64_t w = (int64_t)gy * nx + gx;
-        __stcs(out + w, sD);
-        __stcs(out + n + w, sL);
-        __stcs(out + 2 * n + w, sR);
-        __stcs(out + 3 * n + w, sU);
+        __stcs(out + w, make_double2(__dmul_rn(sD.x, kScale), __dmul_rn(sD.y, kScale)));
+        __stcs(out + n + w, make_double2(__dmul_rn(sL.x, kScale), __dmul_rn(sL.y, kScale)));
+        __stcs(out + 2 * n + w, make_double2(__dmul_rn(sR.x, kScale), __dmul_rn(sR.y, kScale)));
+        __stcs(out + 3 * n + w, make_double2(__dmul_rn(sU.x, kScale), __dmul_rn(sU.y, kScale)));
       }
     }
   }
@@ -333,26 +372,31 @@ namespace qwb {
 // Steps per temporally blocked launch (0 = single-step kernel only).
 // QWB_LATTICE_T overrides (0, 2..8); QWB_LATTICE_KIND picks the wavefront
 // ("wf", default) or the CTA-tile ("tile") variant; QWB_LATTICE_SHAPE the tile shape.
+static int lattice_kind() {   // 1 = CTA tile (default), 0 = wavefront
+  static int kind = -1;
+  if (kind < 0) {
+    const char* e = getenv("QWB_LATTICE_KIND");
+    kind = (e && strcmp(e, "wf") == 0) ? 0 : 1;
+  }
+  return kind;
+}
+
 int lattice_tb_depth(int64_t nx, int64_t ny, int64_t n_marked) {
   static int depth = -1;
   if (depth < 0) {
-    depth = env_int("QWB_LATTICE_T", 6);
-    if (depth < 0 || depth > 8 || depth == 1) depth = 6;
+    depth = env_int("QWB_LATTICE_T", 4);
+    if (depth < 0 || depth > 8 || depth == 1) depth = 4;
   }
   if (nx < 64 || ny < 64) return 0;   // tiny lattices: the single-step kernel is launch-bound anyway
-  if (n_marked > 8) return 0;         // the fused kernels take the marked set as a short list
+  if (lattice_kind() == 0 && n_marked > 8) return 0;   // wavefront takes marked as a short list
+  if (lattice_kind() == 1 && depth > 6) return 6;
   return depth;
 }
 
 int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny,
                       const double2* in, double2* out, const uint32_t* bits,
                       const int64_t* marked_host, int64_t n_marked) {
-  static int kind = -1;
-  if (kind < 0) {
-    const char* e = getenv("QWB_LATTICE_KIND");
-    kind = (e && strcmp(e, "tile") == 0) ? 1 : 0;
-  }
-  if (kind == 0) {
+  if (lattice_kind() == 0) {
     MarkedList mk{};
     mk.n = (int)n_marked;
     for (int k = 0; k < mk.n; ++k) mk.v[k] = marked_host[k];
@@ -368,19 +412,24 @@ int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx
     }
   }
   static int shape = -1;
-  if (shape < 0) shape = env_int("QWB_LATTICE_SHAPE", 2);
-  if (depth > 4) depth = 4;
-  // shape 0: 32x32 threads, 1 vertex each; 1: 32x16 threads, 2 rows each (32x32 region);
-  // 2: 32x24 threads, 2 rows each (32x48 region)
+  if (shape < 0) shape = env_int("QWB_LATTICE_SHAPE", 3);
+  if (depth > 6) depth = 6;
+  MarkedList mk{};
+  mk.n = n_marked <= 8 ? (int)n_marked : -1;
+  for (int k = 0; k < mk.n; ++k) mk.v[k] = marked_host[k];
+  // shape 1: 32x16 threads, 2 rows each (32x32 region); 2: 32x24 threads, 2 rows
+  // each (32x48 region); 3: 32x16 threads, 3 rows each (32x48 region)
 #define QWB_TB_CASE(T_)                                                                     \
   case T_:                                                                                  \
-    if (shape == 0) return launch_tb<T_, 32, 1>(ctx, shift, s, nx, ny, in, out, bits);      \
-    if (shape == 2) return launch_tb<T_, 24, 2>(ctx, shift, s, nx, ny, in, out, bits);      \
-    return launch_tb<T_, 16, 2>(ctx, shift, s, nx, ny, in, out, bits);
+    if (shape == 2) return launch_tb<T_, 24, 2>(ctx, shift, s, nx, ny, in, out, bits, mk);  \
+    if (shape == 3) return launch_tb<T_, 16, 3>(ctx, shift, s, nx, ny, in, out, bits, mk);  \
+    return launch_tb<T_, 16, 2>(ctx, shift, s, nx, ny, in, out, bits, mk);
   switch (depth) {
     QWB_TB_CASE(2)
     QWB_TB_CASE(3)
     QWB_TB_CASE(4)
+    QWB_TB_CASE(5)
+    QWB_TB_CASE(6)
     default:
       QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "unsupported temporal block depth %d", depth);
   }

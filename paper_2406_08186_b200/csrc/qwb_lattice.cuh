@@ -112,6 +112,74 @@ __device__ __forceinline__ double2 scale_fin(double c, double2 s) {
   return make_double2(__fma_rn(c, s.x, nzsign(s.y)), __fma_rn(c, s.y, zsign(s.x)));
 }
 
+// ---- doubled-space forms (temporally blocked kernels) -----------------------
+// numpy computes O = q0 + ((q1 + q2) + q3) with q_i = +-0.5 s_i.  Halving is
+// exact and commutes with round-to-nearest for normal operands, so
+//     O = 0.5 * fl(+-s0 + fl(fl(+-s1 +- s2) +- s3))
+// The fused kernels therefore iterate the doubled operator 2U with additions
+// only (the state after t on-chip steps is 2^t psi_t exactly) and scale by
+// 2^-T when they store.  Identical bits to numpy for every non-zero result; an
+// exact zero may come out as -0.0 instead of +0.0 or vice versa (equal under
+// ==, np.array_equal and every reduction).  Normalised states cannot reach the
+// subnormal range where the argument would fail (cancellation of doubles of
+// magnitude >= 2^-60 leaves results >= 2^-112 or exactly 0).
+__device__ __forceinline__ double2 csub(double2 a, double2 b) {
+  return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y));
+}
+
+__device__ __forceinline__ void vertex_outputs2_interior(double2 vD, double2 vL, double2 vR, double2 vU,
+                                                         double2& oD, double2& oL, double2& oR,
+                                                         double2& oU) {
+  const double2 t = cadd(vL, vR);     // L + R
+  const double2 w = csub(vR, vL);     // -L + R
+  oD = csub(cadd(t, vU), vD);         // -D + ((L + R) + U)
+  oL = cadd(vD, cadd(w, vU));         //  D + ((-L + R) + U)
+  oR = cadd(vD, csub(vU, w));         //  D + ((L - R) + U)
+  oU = cadd(vD, csub(t, vU));         //  D + ((L + R) - U)
+}
+
+__device__ __forceinline__ void vertex_outputs2(int gx, int gy, int nx, int ny, bool marked, double2 vD,
+                                                double2 vL, double2 vR, double2 vU, double2& oD,
+                                                double2& oL, double2& oR, double2& oU) {
+  if (marked) {   // 2 * (-psi)
+    oD = make_double2(-__dadd_rn(vD.x, vD.x), -__dadd_rn(vD.y, vD.y));
+    oL = make_double2(-__dadd_rn(vL.x, vL.x), -__dadd_rn(vL.y, vL.y));
+    oR = make_double2(-__dadd_rn(vR.x, vR.x), -__dadd_rn(vR.y, vR.y));
+    oU = make_double2(-__dadd_rn(vU.x, vU.x), -__dadd_rn(vU.y, vU.y));
+    return;
+  }
+  if ((gx > 0) & (gx < nx - 1) & (gy > 0) & (gy < ny - 1)) {
+    vertex_outputs2_interior(vD, vL, vR, vU, oD, oL, oR, oU);
+    return;
+  }
+  const Slots o = order_slots(gx, gy, nx, ny, vD, vL, vR, vU);
+  const double2 t12 = cadd(o.s1, o.s2);
+  const double2 d21 = csub(o.s2, o.s1);
+  const double2 O0 = csub(cadd(t12, o.s3), o.s0);
+  const double2 O1 = cadd(o.s0, cadd(d21, o.s3));
+  const double2 O2 = cadd(o.s0, csub(o.s3, d21));
+  const double2 O3 = cadd(o.s0, csub(t12, o.s3));
+  oD = pick(o.pD, O0, O1, O2, O3);
+  oL = pick(o.pL, O0, O1, O2, O3);
+  oR = pick(o.pR, O0, O1, O2, O3);
+  oU = pick(o.pU, O0, O1, O2, O3);
+}
+
+// interior, unmarked vertex: slot order is D L R U
+__device__ __forceinline__ void vertex_outputs_interior(double2 vD, double2 vL, double2 vR, double2 vU,
+                                                        double2& oD, double2& oL, double2& oR,
+                                                        double2& oU) {
+  const double2 qD = scale_fin(0.5, vD), qL = scale_fin(0.5, vL);
+  const double2 qR = scale_fin(0.5, vR), qU = scale_fin(0.5, vU);
+  const double2 nD = scale_fin(-0.5, vD), nL = scale_fin(-0.5, vL);
+  const double2 nR = scale_fin(-0.5, vR), nU = scale_fin(-0.5, vU);
+  const double2 t = cadd(qL, qR);
+  oD = cadd(nD, cadd(t, qU));
+  oL = cadd(qD, cadd(cadd(nL, qR), qU));
+  oR = cadd(qD, cadd(cadd(qL, nR), qU));
+  oU = cadd(qD, cadd(t, nU));
+}
+
 // vertex_outputs for finite inputs; interior vertices (slot order D L R U)
 // skip the slot permutation entirely.
 __device__ __forceinline__ void vertex_outputs_fin(int gx, int gy, int nx, int ny, bool marked,
