@@ -70,6 +70,7 @@ SIGNATURES = {
     "qwb_lattice_from_planes": [_vp, _i64, _i64, _vp, _vp, _vp],
     "qwb_lattice_run": [_vp, _i64, _i64, _i32, _vp, _p_i64, _i64, _vp, _vp, _i64, _p_i64, _i32, _vp,
                         _p_int, _vp],
+    "qwb_lattice_fused_depth": [_i64, _i64, _i64, _p_int, _p_int],
     "qwb_lattice_step": [_vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _vp],
     "qwb_lattice_probability": [_vp, _i64, _i64, _vp, _vp, _vp],
     "qwb_slab_to_planes": [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp],

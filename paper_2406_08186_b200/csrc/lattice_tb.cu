@@ -372,7 +372,7 @@ namespace qwb {
 // Steps per temporally blocked launch (0 = single-step kernel only).
 // QWB_LATTICE_T overrides (0, 2..8); QWB_LATTICE_KIND picks the wavefront
 // ("wf", default) or the CTA-tile ("tile") variant; QWB_LATTICE_SHAPE the tile shape.
-static int lattice_kind() {   // 1 = CTA tile (default), 0 = wavefront
+int lattice_kind() {   // 1 = CTA tile (default), 0 = wavefront
   static int kind = -1;
   if (kind < 0) {
     const char* e = getenv("QWB_LATTICE_KIND");
@@ -437,3 +437,10 @@ int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx
 }
 
 }  // namespace qwb
+
+extern "C" int qwb_lattice_fused_depth(int64_t nx, int64_t ny, int64_t n_marked, int* depth_host,
+                                       int* kind_host) {
+  if (depth_host) *depth_host = qwb::lattice_tb_depth(nx, ny, n_marked);
+  if (kind_host) *kind_host = qwb::lattice_kind();
+  return QWB_OK;
+}

@@ -227,6 +227,7 @@ void lattice_launch(int shift, cudaStream_t s, const Geom& g, const Rows& r, con
 int lattice_check_shift(qwb_ctx* ctx, int shift);
 // temporally blocked single-GPU torus steps (lattice_tb.cu)
 int lattice_tb_depth(int64_t nx, int64_t ny, int64_t n_marked);
+int lattice_kind();   // 1 = CTA-tile kernel, 0 = wavefront kernel
 int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny,
                       const double2* in, double2* out, const uint32_t* bits,
                       const int64_t* marked_host, int64_t n_marked);
