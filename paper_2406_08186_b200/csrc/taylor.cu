@@ -264,6 +264,122 @@ hc_term_kernel(HcTile<MAXD> op, int64_t n, const double2* __restrict__ tin, doub
   }
 }
 
+// ---------------------------------------------------------------------------
+// Hypercube term, positional form (dim >= 10).  The row's columns in ascending
+// order are v with its set bits cleared high->low, then v with its clear bits
+// set low->high.  The kernel walks the ROW POSITIONS p = 0..dim-1 at compile
+// time and finds, per lane, the bit that lands at p with two running masks
+// (clz on the remaining set bits, ffs on the remaining clear bits) — so the
+// numpy pairwise slot of every element, (p-1) % 4, is a compile-time register
+// and no data-dependent control flow remains.  Neighbour values are read-only
+// cached gathers (the 2^b partner of a warp is one contiguous 512-B block).
+// Warps that contain a marked vertex (row length dim+1) use the generic path.
+// ---------------------------------------------------------------------------
+template <int MAXD>
+struct HcPos {
+  int dim;
+  double gamma;
+  const uint32_t* __restrict__ bits;
+};
+
+template <int MAXD>
+__global__ void __launch_bounds__(kTermThreads)
+hc_pos_kernel(HcPos<MAXD> op, int64_t n, const double2* __restrict__ tin, double2* __restrict__ tout,
+              const double2* acc_in, double2* acc_out, double s_k, const int* __restrict__ done,
+              double* __restrict__ partial) {
+  if (*done) return;
+  __shared__ double sh[kTermThreads];
+  const int dim = op.dim;
+  const double2 alpha = make_double2(0.0, -s_k);   // Python complex(-1j * tau / k)
+  const double2 one = make_double2(1.0, 0.0);
+  const double2 g = make_double2(-op.gamma, 0.0);
+  const int m = dim - 1;                            // rest elements after x0
+  const int main_end = m - (m % 4);
+  const unsigned all = (dim >= 32) ? 0xffffffffu : ((1u << dim) - 1u);
+  double nrm = 0.0;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const bool mk = op.bits && ((__ldg(op.bits + (v >> 5)) >> (v & 31)) & 1u);
+    double2 h;
+    if (__any_sync(0xffffffffu, mk)) {
+      StreamRow sr;
+      sr.init(dim + (mk ? 1 : 0));
+      for (int b = dim - 1; b >= 0; --b)
+        if ((v >> b) & 1) sr.push(cmul_np(g, __ldg(tin + (v ^ (1LL << b)))));
+      if (mk) sr.push(cmul_np(make_double2(-1.0, 0.0), __ldg(tin + v)));
+      for (int b = 0; b < dim; ++b)
+        if (!((v >> b) & 1)) sr.push(cmul_np(g, __ldg(tin + (v ^ (1LL << b)))));
+      h = sr.result();
+    } else {
+      const unsigned vb = (unsigned)v & all;
+      unsigned setm = vb, clrm = (~vb) & all;
+      const int pc = __popc(vb);
+      // (the compiler's own interleaving of the gathers with the ordered sum
+      // measured best: 74 registers, 3 CTAs/SM; explicit all-loads-first or a
+      // register prefetch ring raised register use and lost occupancy)
+      double2 x0 = make_double2(0.0, 0.0), c0 = x0, c1 = x0, c2 = x0, c3 = x0;
+      double2 tl0 = x0, tl1 = x0, tl2 = x0;
+#pragma unroll
+      for (int p = 0; p < MAXD; ++p) {
+        if (p < dim) {
+          const int bs = 31 - __clz(setm | 1u);
+          const int bc = __ffs(clrm | 0x80000000u) - 1;
+          const bool use_set = p < pc;
+          const int b = use_set ? bs : bc;
+          setm = use_set ? (setm ^ (1u << bs)) : setm;
+          clrm = use_set ? clrm : (clrm ^ (1u << bc));
+          const double2 e = cmul_np(g, __ldg(tin + (v ^ (1LL << b))));
+          if (p == 0) {
+            x0 = e;
+          } else {
+            const int i = p - 1;
+            if (i < main_end) {
+              double2& c = (i % 4 == 0) ? c0 : (i % 4 == 1) ? c1 : (i % 4 == 2) ? c2 : c3;
+              c = (i < 4) ? e : cadd(c, e);
+            } else {
+              const int k = i - main_end;   // 0..2, uniform
+              tl0 = (k == 0) ? e : tl0;
+              tl1 = (k == 1) ? e : tl1;
+              tl2 = (k == 2) ? e : tl2;
+            }
+          }
+        }
+      }
+      double2 r;
+      if (m < 4) {
+        r = make_double2(-0.0, -0.0);
+        if (m > 0) r = cadd(r, c0);
+        if (m > 1) r = cadd(r, c1);
+        if (m > 2) r = cadd(r, c2);
+      } else {
+        r = cadd(cadd(c0, c1), cadd(c2, c3));
+        const int tail = m - main_end;
+        if (tail > 0) r = cadd(r, tl0);
+        if (tail > 1) r = cadd(r, tl1);
+        if (tail > 2) r = cadd(r, tl2);
+      }
+      h = cadd(x0, r);
+    }
+    const double2 t = cmul_np(alpha, h);
+    tout[v] = t;
+    acc_out[v] = cadd(acc_in[v], cmul_np(one, t));
+    nrm = __fma_rn(t.x, t.x, __fma_rn(t.y, t.y, nrm));
+  }
+  sh[threadIdx.x] = nrm;
+  __syncthreads();
+  for (int s = kTermThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+template <int MAXD>
+void launch_term(const HcPos<MAXD>& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
+                 const double2* ain, double2* acc, double s_k, const int* flags, double* partial) {
+  hc_pos_kernel<MAXD><<<kTermBlocks, kTermThreads, 0, s>>>(op, n, tin, tout, ain, acc, s_k, flags, partial);
+}
+
 template <class Op>
 void launch_term(const Op& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
                  const double2* ain, double2* acc, double s_k, const int* flags, double* partial) {
@@ -363,16 +479,29 @@ int qwb_taylor_evolve_hypercube(qwb_ctx* ctx, int dim, double gamma, const uint3
   double2* p = reinterpret_cast<double2*>(psi);
   double2* w = reinterpret_cast<double2*>(work);
   cudaStream_t s = qwb::as_stream(stream);
-  static int tiled = -1;   // QWB_HC_TILED=0 selects the per-thread gather kernel
+  // QWB_HC_KERNEL: 2 = positional (default), 1 = subcube tile, 0 = generic gather
+  static int tiled = -1;
   if (tiled < 0) {
-    const char* e = getenv("QWB_HC_TILED");
-    tiled = (e && *e == '0') ? 0 : 1;
+    const char* e = getenv("QWB_HC_KERNEL");
+    tiled = (e && *e) ? atoi(e) : 2;
   }
   if (dim <= 8) {
     HypercubeOp<8> op{dim, gamma, marked_bits};
     return evolve(ctx, op, n, p, w, substeps, tau, floor, max_terms, terms_host, s);
   }
-  if (tiled) {
+  if (tiled == 2 && dim >= 10) {
+    if (dim <= 16) {
+      HcPos<16> op{dim, gamma, marked_bits};
+      return evolve(ctx, op, n, p, w, substeps, tau, floor, max_terms, terms_host, s);
+    }
+    if (dim <= 24) {
+      HcPos<24> op{dim, gamma, marked_bits};
+      return evolve(ctx, op, n, p, w, substeps, tau, floor, max_terms, terms_host, s);
+    }
+    HcPos<31> op{dim, gamma, marked_bits};
+    return evolve(ctx, op, n, p, w, substeps, tau, floor, max_terms, terms_host, s);
+  }
+  if (tiled == 1) {
     if (dim <= 16) {
       HcTile<16> op{dim, gamma, marked_bits};
       return evolve(ctx, op, n, p, w, substeps, tau, floor, max_terms, terms_host, s);
