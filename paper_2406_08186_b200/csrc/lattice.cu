@@ -347,11 +347,13 @@ int qwb_lattice_run(qwb_ctx* ctx, int64_t nx, int64_t ny, int shift, const uint3
   // T coined steps per HBM pass when no per-step trace is requested
   if (n_marked > 0 && (!marked_bits || !marked_host))
     QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "marked vertices need both the bitmap and the host list");
-  const int depth = trace ? 0 : qwb::lattice_tb_depth(nx, ny, n_marked);
+  // the tile kernel fuses the per-step trace too; the wavefront kernel does not
+  const int depth = (trace && qwb::lattice_kind() == 0) ? 0 : qwb::lattice_tb_depth(nx, ny, n_marked);
   if (depth > 0) {
     for (; k + depth <= steps; k += depth) {
       st = qwb::lattice_tb_launch(ctx, depth, shift, s, (int)nx, (int)ny, cur, nxt, marked_bits,
-                                  marked_host, n_marked);
+                                  marked_host, n_marked, trace_vertices_host, trace ? n_trace : 0,
+                                  trace ? trace + k * n_trace : nullptr);
       if (st) return st;
       double2* t = cur;
       cur = nxt;

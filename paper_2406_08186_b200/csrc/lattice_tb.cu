@@ -55,13 +55,23 @@ struct TbShape {
   static constexpr size_t smem_bytes() { return (4 * (size_t)REG + 4 * (size_t)NT) * sizeof(double2); }
 };
 
+// p(v) per step for up to 8 traced vertices (search runs): out[t * n + k]
+struct TraceList {
+  int n;
+  int64_t v[8];
+  double* out;
+};
+
 // T steps of a tile on chip (see the file comment).  INTERIOR: every vertex of
-// the region is an unmarked interior vertex (no slot permutation, no branches).
-template <int SHIFT, bool MARKED, int T, int BY, int V, bool INTERIOR>
+// the region is an unmarked, untraced interior vertex (no slot permutation, no
+// branches).  TRACE: emit p of the state before each step for traced vertices
+// this tile owns (the exact inner block), unscaled from doubled space.
+template <int SHIFT, bool MARKED, int T, int BY, int V, bool INTERIOR, bool TRACE>
 __device__ __forceinline__ void tile_steps(int nx, int ny, int gx, const int (&gy)[V],
                                            const uint32_t* __restrict__ bits, double2 (&vD)[V],
                                            double2 (&vL)[V], double2 (&vR)[V], double2 (&vU)[V],
-                                           double2* xD, double2* xU, int tid, int ty) {
+                                           double2* xD, double2* xU, int tid, int ty,
+                                           const TraceList& tr, const bool (&own)[V]) {
   bool mk[V];
 #pragma unroll
   for (int j = 0; j < V; ++j) {
@@ -73,6 +83,22 @@ __device__ __forceinline__ void tile_steps(int nx, int ny, int gx, const int (&g
   }
 #pragma unroll
   for (int t = 0; t < T; ++t) {
+    if (TRACE) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        if (!own[j]) continue;
+        const int64_t wg = (int64_t)gy[j] * nx + gx;
+        for (int k = 0; k < tr.n; ++k) {
+          if (tr.v[k] != wg) continue;
+          const double sc = 1.0 / (double)(1 << t);   // level t holds 2^t psi_t
+          const auto un = [&](double2 a) { return make_double2(__dmul_rn(a.x, sc), __dmul_rn(a.y, sc)); };
+          const qwb::Slots o = qwb::order_slots(gx, gy[j], nx, ny, un(vD[j]), un(vL[j]), un(vR[j]), un(vU[j]));
+          const double m0 = qwb::abs2_np(o.s0), m1 = qwb::abs2_np(o.s1), m2 = qwb::abs2_np(o.s2),
+                       m3 = qwb::abs2_np(o.s3);
+          tr.out[t * tr.n + k] = __dadd_rn(m0, __dadd_rn(__dadd_rn(m1, m2), m3));
+        }
+      }
+    }
     double2 oD[V], oL[V], oR[V], oU[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) {
@@ -118,7 +144,8 @@ struct MarkedList {   // up to 8 marked vertex ids; n < 0: more than 8 (use the 
 template <int SHIFT, bool MARKED, int T, int BY, int V>
 __global__ void __launch_bounds__(32 * BY, 1)
 lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __restrict__ out,
-                  const uint32_t* __restrict__ bits, MarkedList mk, int tiles_x, int ntiles) {
+                  const uint32_t* __restrict__ bits, MarkedList mk, TraceList tr, int tiles_x,
+                  int ntiles) {
   using S = TbShape<BY, V>;
   constexpr int OX = S::RX - 2 * T, OY = S::RY - 2 * T;   // exact (owned) block
   extern __shared__ double2 sm[];
@@ -166,30 +193,42 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
     __syncthreads();
     if (tile + (int)gridDim.x < ntiles) prefetch(tile + gridDim.x);
     cp_commit();
-    // regions that touch no torus edge and hold no marked vertex run a
-    // branch-free specialisation: every vertex is interior (slot order D L R U)
+    // regions that touch no torus edge and hold no marked or traced vertex run
+    // a branch-free specialisation: every vertex is interior (slot order D L R U)
+    auto in_region = [&](int64_t w) {
+      const int mx = (int)(w % nx), my = (int)(w / nx);
+      return mx >= x0 - T && mx < x0 - T + 32 && my >= y0 - T && my < y0 - T + S::RY;
+    };
     bool interior = x0 - T >= 1 && x0 - T + 31 <= nx - 2 && y0 - T >= 1 &&
                     y0 - T + S::RY - 1 <= ny - 2;
     if (MARKED && interior) {
       if (mk.n < 0) {
         interior = false;   // too many marked vertices for the list: general path
       } else {
-        for (int k = 0; k < mk.n; ++k) {
-          const int mx = (int)(mk.v[k] % nx), my = (int)(mk.v[k] / nx);
-          interior &= !(mx >= x0 - T && mx < x0 - T + 32 && my >= y0 - T && my < y0 - T + S::RY);
-        }
+        for (int k = 0; k < mk.n; ++k) interior &= !in_region(mk.v[k]);
       }
     }
-    if (interior)
-      tile_steps<SHIFT, false, T, BY, V, true>(nx, ny, gx, gy, bits, vD, vL, vR, vU, xD, xU, tid, ty);
-    else
-      tile_steps<SHIFT, MARKED, T, BY, V, false>(nx, ny, gx, gy, bits, vD, vL, vR, vU, xD, xU, tid, ty);
+    for (int k = 0; k < tr.n; ++k) interior &= !in_region(tr.v[k]);
     const bool col_ok = tx >= T && tx < T + OX && x0 + tx - T < nx;
-    constexpr double kScale = 1.0 / (double)(1 << T);   // undo the doubled-space steps (exact)
+    bool own[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       const int ly = ty * V + j;
-      if (col_ok && ly >= T && ly < T + OY && y0 + ly - T < ny) {
+      own[j] = col_ok && ly >= T && ly < T + OY && y0 + ly - T < ny;
+    }
+    if (interior)
+      tile_steps<SHIFT, false, T, BY, V, true, false>(nx, ny, gx, gy, bits, vD, vL, vR, vU, xD, xU,
+                                                      tid, ty, tr, own);
+    else if (tr.n > 0)
+      tile_steps<SHIFT, MARKED, T, BY, V, false, true>(nx, ny, gx, gy, bits, vD, vL, vR, vU, xD, xU,
+                                                       tid, ty, tr, own);
+    else
+      tile_steps<SHIFT, MARKED, T, BY, V, false, false>(nx, ny, gx, gy, bits, vD, vL, vR, vU, xD, xU,
+                                                        tid, ty, tr, own);
+    constexpr double kScale = 1.0 / (double)(1 << T);   // undo the doubled-space steps (exact)
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      if (own[j]) {
         const int64_t w = (int64_t)gy[j] * nx + gx;
         __stcs(out + w, make_double2(__dmul_rn(vD[j].x, kScale), __dmul_rn(vD[j].y, kScale)));
         __stcs(out + n + w, make_double2(__dmul_rn(vL[j].x, kScale), __dmul_rn(vL[j].y, kScale)));
@@ -203,7 +242,7 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
 
 template <int SHIFT, bool MARKED, int T, int BY, int V>
 int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const double2* in, double2* out,
-                const uint32_t* bits, const MarkedList& mk) {
+                const uint32_t* bits, const MarkedList& mk, const TraceList& tr) {
   using Sh = TbShape<BY, V>;
   constexpr int OX = Sh::RX - 2 * T, OY = Sh::RY - 2 * T;
   const int tiles_x = (nx + OX - 1) / OX, tiles_y = (ny + OY - 1) / OY;
@@ -219,19 +258,19 @@ int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const double2* in,
   }
   const int grid = ntiles < ctx->num_sms ? ntiles : ctx->num_sms;
   lattice_tb_kernel<SHIFT, MARKED, T, BY, V><<<grid, dim3(32, BY), smem, s>>>(nx, ny, in, out, bits,
-                                                                               mk, tiles_x, ntiles);
+                                                                               mk, tr, tiles_x, ntiles);
   return QWB_OK;
 }
 
 template <int T, int BY, int V>
 int launch_tb(qwb_ctx* ctx, int shift, cudaStream_t s, int nx, int ny, const double2* in,
-              double2* out, const uint32_t* bits, const MarkedList& mk) {
+              double2* out, const uint32_t* bits, const MarkedList& mk, const TraceList& tr) {
   if (shift == QWB_SHIFT_FLIPFLOP) {
-    return bits ? launch_tb_t<QWB_SHIFT_FLIPFLOP, true, T, BY, V>(ctx, s, nx, ny, in, out, bits, mk)
-                : launch_tb_t<QWB_SHIFT_FLIPFLOP, false, T, BY, V>(ctx, s, nx, ny, in, out, bits, mk);
+    return bits ? launch_tb_t<QWB_SHIFT_FLIPFLOP, true, T, BY, V>(ctx, s, nx, ny, in, out, bits, mk, tr)
+                : launch_tb_t<QWB_SHIFT_FLIPFLOP, false, T, BY, V>(ctx, s, nx, ny, in, out, bits, mk, tr);
   }
-  return bits ? launch_tb_t<QWB_SHIFT_PERSISTENT, true, T, BY, V>(ctx, s, nx, ny, in, out, bits, mk)
-              : launch_tb_t<QWB_SHIFT_PERSISTENT, false, T, BY, V>(ctx, s, nx, ny, in, out, bits, mk);
+  return bits ? launch_tb_t<QWB_SHIFT_PERSISTENT, true, T, BY, V>(ctx, s, nx, ny, in, out, bits, mk, tr)
+              : launch_tb_t<QWB_SHIFT_PERSISTENT, false, T, BY, V>(ctx, s, nx, ny, in, out, bits, mk, tr);
 }
 
 int env_int(const char* name, int dflt) {
@@ -395,8 +434,10 @@ int lattice_tb_depth(int64_t nx, int64_t ny, int64_t n_marked) {
 
 int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny,
                       const double2* in, double2* out, const uint32_t* bits,
-                      const int64_t* marked_host, int64_t n_marked) {
+                      const int64_t* marked_host, int64_t n_marked,
+                      const int64_t* trace_vertices_host, int n_trace, double* trace) {
   if (lattice_kind() == 0) {
+    if (trace) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "the wavefront kernel does not fuse traces");
     MarkedList mk{};
     mk.n = (int)n_marked;
     for (int k = 0; k < mk.n; ++k) mk.v[k] = marked_host[k];
@@ -417,13 +458,17 @@ int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx
   MarkedList mk{};
   mk.n = n_marked <= 8 ? (int)n_marked : -1;
   for (int k = 0; k < mk.n; ++k) mk.v[k] = marked_host[k];
+  TraceList tl{};
+  tl.n = trace ? n_trace : 0;
+  tl.out = trace;
+  for (int k = 0; k < tl.n; ++k) tl.v[k] = trace_vertices_host[k];
   // shape 1: 32x16 threads, 2 rows each (32x32 region); 2: 32x24 threads, 2 rows
   // each (32x48 region); 3: 32x16 threads, 3 rows each (32x48 region)
-#define QWB_TB_CASE(T_)                                                                     \
-  case T_:                                                                                  \
-    if (shape == 2) return launch_tb<T_, 24, 2>(ctx, shift, s, nx, ny, in, out, bits, mk);  \
-    if (shape == 3) return launch_tb<T_, 16, 3>(ctx, shift, s, nx, ny, in, out, bits, mk);  \
-    return launch_tb<T_, 16, 2>(ctx, shift, s, nx, ny, in, out, bits, mk);
+#define QWB_TB_CASE(T_)                                                                        \
+  case T_:                                                                                     \
+    if (shape == 2) return launch_tb<T_, 24, 2>(ctx, shift, s, nx, ny, in, out, bits, mk, tl); \
+    if (shape == 3) return launch_tb<T_, 16, 3>(ctx, shift, s, nx, ny, in, out, bits, mk, tl); \
+    return launch_tb<T_, 16, 2>(ctx, shift, s, nx, ny, in, out, bits, mk, tl);
   switch (depth) {
     QWB_TB_CASE(2)
     QWB_TB_CASE(3)

@@ -230,7 +230,8 @@ int lattice_tb_depth(int64_t nx, int64_t ny, int64_t n_marked);
 int lattice_kind();   // 1 = CTA-tile kernel, 0 = wavefront kernel
 int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny,
                       const double2* in, double2* out, const uint32_t* bits,
-                      const int64_t* marked_host, int64_t n_marked);
+                      const int64_t* marked_host, int64_t n_marked,
+                      const int64_t* trace_vertices_host, int n_trace, double* trace);
 int lattice_slab_geom(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, Geom* g);
 // part: 0 = all owned rows, 1 = first and last owned rows, 2 = interior owned rows
 Rows slab_rows(int64_t ny_local, int part);
