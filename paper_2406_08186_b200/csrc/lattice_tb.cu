@@ -141,7 +141,7 @@ struct MarkedList {   // up to 8 marked vertex ids; n < 0: more than 8 (use the 
   int64_t v[8];
 };
 
-template <int SHIFT, bool MARKED, int T, int BY, int V>
+template <int SHIFT, bool MARKED, int T, int BY, int V, bool TRACE>
 __global__ void __launch_bounds__(32 * BY, 1)
 lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __restrict__ out,
                   const uint32_t* __restrict__ bits, MarkedList mk, TraceList tr, int tiles_x,
@@ -208,7 +208,8 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
         for (int k = 0; k < mk.n; ++k) interior &= !in_region(mk.v[k]);
       }
     }
-    for (int k = 0; k < tr.n; ++k) interior &= !in_region(tr.v[k]);
+    if (TRACE)
+      for (int k = 0; k < tr.n; ++k) interior &= !in_region(tr.v[k]);
     const bool col_ok = tx >= T && tx < T + OX && x0 + tx - T < nx;
     bool own[V];
 #pragma unroll
@@ -219,11 +220,8 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
     if (interior)
       tile_steps<SHIFT, false, T, BY, V, true, false>(nx, ny, gx, gy, bits, vD, vL, vR, vU, xD, xU,
                                                       tid, ty, tr, own);
-    else if (tr.n > 0)
-      tile_steps<SHIFT, MARKED, T, BY, V, false, true>(nx, ny, gx, gy, bits, vD, vL, vR, vU, xD, xU,
-                                                       tid, ty, tr, own);
     else
-      tile_steps<SHIFT, MARKED, T, BY, V, false, false>(nx, ny, gx, gy, bits, vD, vL, vR, vU, xD, xU,
+      tile_steps<SHIFT, MARKED, T, BY, V, false, TRACE>(nx, ny, gx, gy, bits, vD, vL, vR, vU, xD, xU,
                                                         tid, ty, tr, own);
     constexpr double kScale = 1.0 / (double)(1 << T);   // undo the doubled-space steps (exact)
 #pragma unroll
@@ -248,18 +246,20 @@ int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const double2* in,
   const int tiles_x = (nx + OX - 1) / OX, tiles_y = (ny + OY - 1) / OY;
   const int ntiles = tiles_x * tiles_y;
   const size_t smem = Sh::smem_bytes();
-  static bool configured[256] = {};   // per instantiation and device
-  const int dev = ctx->device & 255;
-  if (!configured[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(lattice_tb_kernel<SHIFT, MARKED, T, BY, V>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return qwb::cuda_status(ctx, e, "cudaFuncSetAttribute(lattice_tb)");
-    configured[dev] = true;
-  }
   const int grid = ntiles < ctx->num_sms ? ntiles : ctx->num_sms;
-  lattice_tb_kernel<SHIFT, MARKED, T, BY, V><<<grid, dim3(32, BY), smem, s>>>(nx, ny, in, out, bits,
-                                                                               mk, tr, tiles_x, ntiles);
-  return QWB_OK;
+  auto go = [&](auto kernel, bool* configured) -> int {
+    const int dev = ctx->device & 255;
+    if (!configured[dev]) {
+      cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return qwb::cuda_status(ctx, e, "cudaFuncSetAttribute(lattice_tb)");
+      configured[dev] = true;
+    }
+    kernel<<<grid, dim3(32, BY), smem, s>>>(nx, ny, in, out, bits, mk, tr, tiles_x, ntiles);
+    return QWB_OK;
+  };
+  static bool conf_plain[256] = {}, conf_trace[256] = {};   // per instantiation and device
+  if (tr.n > 0) return go(lattice_tb_kernel<SHIFT, MARKED, T, BY, V, true>, conf_trace);
+  return go(lattice_tb_kernel<SHIFT, MARKED, T, BY, V, false>, conf_plain);
 }
 
 template <int T, int BY, int V>
