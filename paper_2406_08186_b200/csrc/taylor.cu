@@ -374,22 +374,390 @@ hc_pos_kernel(HcPos<MAXD> op, int64_t n, const double2* __restrict__ tin, double
   if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
 }
 
+// ---------------------------------------------------------------------------
+// Hypercube term, TMA-streamed form (dim >= 10).  A CTA owns tiles of 1024
+// consecutive vertices (bits 0..9); every neighbour of a tile across a high
+// bit b >= 10 lies in ONE contiguous 16-KB partner tile (tile ^ 2^(b-10)).
+// Row v's ascending column order is: high set bits (descending), then the 10
+// low bits (lane-dependent order), then high clear bits (ascending) — the
+// high-bit positions are the same for the whole tile.  So a producer warp
+// streams, per tile, the partner tiles in row-position order (the tile itself
+// at the position of the low segment) with 1-D bulk copies
+// (cp.async.bulk + mbarrier complete_tx) into a ring of shared-memory stages,
+// and the consumer threads fold each stage into the numpy pairwise
+// accumulators of their vertices in order: every global read is a 16-KB bulk
+// transfer, no gather, no long-scoreboard stall on the compute warps.
+// Vertices of marked rows (diagonal entry, row length dim+1) are recomputed by
+// the generic ordered row after the stream (rare).
+// ---------------------------------------------------------------------------
+namespace hcs {
+constexpr int LB = 10;                     // low bits per tile
+constexpr int TILE = 1 << LB;              // vertices per tile
+constexpr uint32_t CHUNK_BYTES = TILE * sizeof(double2);
+// NS ring stages + a double-buffered acc tile + barriers
+constexpr size_t smem_bytes(int ns) { return (size_t)(ns + 2) * CHUNK_BYTES + (2 * ns + 4) * sizeof(uint64_t); }
+}  // namespace hcs
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "HCS_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra HCS_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// (c + 0i) * x in numpy's FMA form for finite x: the 0*x terms are signed
+// zeros, produced with bit operations (exactly what the FP multiply returns).
+__device__ __forceinline__ double2 scale_real_fin(double c, double2 x) {
+  const long long sx = __double_as_longlong(x.x) & (long long)0x8000000000000000ULL;
+  const long long sy = __double_as_longlong(x.y) & (long long)0x8000000000000000ULL;
+  return make_double2(__fma_rn(c, x.x, __longlong_as_double(sy ^ (long long)0x8000000000000000ULL)),
+                      __fma_rn(c, x.y, __longlong_as_double(sx)));
+}
+
+// numpy x0 + pairwise(x1..x_m), 4 <= m < 64, for VPT rows whose element
+// positions agree (warp-uniform slot): x0, then accumulators c0..c3 take
+// elements 1 + 4q + j, the tail (elements after main_end) is added to the
+// combined (c0 + c1) + (c2 + c3).  Accumulators start at -0.0, so the first
+// addition returns the element itself bit for bit (signed zeros included).
+// slot: 0 = x0, 1..4 = c0..c3, 5 = first tail element, 6 = later tail.
+__device__ __forceinline__ int pos_slot(int p, int main_end) {
+  if (p == 0) return 0;
+  const int i = p - 1;
+  if (i < main_end) return 1 + (i & 3);
+  return i == main_end ? 5 : 6;
+}
+
+template <int V>
+struct PosAccs {
+  double2 x0[V], c0[V], c1[V], c2[V], c3[V];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int j = 0; j < V; ++j) x0[j] = c0[j] = c1[j] = c2[j] = c3[j] = make_double2(-0.0, -0.0);
+  }
+  __device__ __forceinline__ void push(int slot, const double2 (&e)[V]) {
+    switch (slot) {
+      case 0:
+#pragma unroll
+        for (int j = 0; j < V; ++j) x0[j] = cadd(x0[j], e[j]);
+        break;
+      case 1:
+#pragma unroll
+        for (int j = 0; j < V; ++j) c0[j] = cadd(c0[j], e[j]);
+        break;
+      case 2:
+#pragma unroll
+        for (int j = 0; j < V; ++j) c1[j] = cadd(c1[j], e[j]);
+        break;
+      case 3:
+#pragma unroll
+        for (int j = 0; j < V; ++j) c2[j] = cadd(c2[j], e[j]);
+        break;
+      case 4:
+#pragma unroll
+        for (int j = 0; j < V; ++j) c3[j] = cadd(c3[j], e[j]);
+        break;
+      case 5:
+#pragma unroll
+        for (int j = 0; j < V; ++j) c0[j] = cadd(cadd(cadd(c0[j], c1[j]), cadd(c2[j], c3[j])), e[j]);
+        break;
+      default:
+#pragma unroll
+        for (int j = 0; j < V; ++j) c0[j] = cadd(c0[j], e[j]);
+        break;
+    }
+  }
+  __device__ __forceinline__ double2 result(int j, int m, int main_end) const {
+    const double2 r = (m == main_end) ? cadd(cadd(c0[j], c1[j]), cadd(c2[j], c3[j])) : c0[j];
+    return cadd(x0[j], r);
+  }
+};
+
+// marked row v: -1 * psi[v] sits between the set and the clear neighbours
+// (row length dim + 1); out of line so the streaming loop keeps its registers
+__device__ __noinline__ double2 hc_marked_row(int dim, double g, const double2* __restrict__ tin, int64_t v) {
+  StreamRow sr;
+  sr.init(dim + 1);
+  const double2 gg = make_double2(g, 0.0);
+  for (int b = dim - 1; b >= 0; --b)
+    if ((v >> b) & 1) sr.push(cmul_np(gg, __ldg(tin + (v ^ (1LL << b)))));
+  sr.push(cmul_np(make_double2(-1.0, 0.0), __ldg(tin + v)));
+  for (int b = 0; b < dim; ++b)
+    if (!((v >> b) & 1)) sr.push(cmul_np(gg, __ldg(tin + (v ^ (1LL << b)))));
+  return sr.result();
+}
+
+struct HcStream {
+  int dim;
+  double gamma;
+  const uint32_t* __restrict__ bits;
+  int grid;
+  int device;
+  int variant;
+};
+
+// NS: ring stages; SPLIT: producer lanes, each copying 1/SPLIT of a chunk;
+// CONS: consumer threads (+ one producer warp), TILE / CONS vertices each
+template <int NS, int SPLIT, int CONS>
+__global__ void __launch_bounds__(CONS + 32, 1)
+hc_stream_kernel(HcStream op, int64_t n, const double2* __restrict__ tin, double2* __restrict__ tout,
+                 const double2* acc_in, double2* acc_out, double s_k, const int* __restrict__ done,
+                 double* __restrict__ partial) {
+  using namespace hcs;
+  constexpr int VPT = TILE / CONS;
+  if (*done) return;
+  extern __shared__ __align__(128) unsigned char hcs_smem[];
+  double2* ring = reinterpret_cast<double2*>(hcs_smem);
+  double2* accbuf = ring + (size_t)NS * TILE;                  // [2][TILE]
+  uint64_t* full = reinterpret_cast<uint64_t*>(hcs_smem + (size_t)(NS + 2) * CHUNK_BYTES);
+  uint64_t* empty = full + NS;
+  uint64_t* afull = empty + NS;                                // [2]
+  uint64_t* aempty = afull + 2;                                // [2]
+  __shared__ double red[CONS / 32 + 1];
+  const int tid = threadIdx.x;
+  const int dim = op.dim;
+  const int nh = dim - LB;                            // high bits
+  const uint32_t hmask = (nh >= 32) ? 0xffffffffu : ((1u << nh) - 1u);
+  const int64_t ntiles = n >> LB;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, CONS / 32);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(afull + s, 1);
+      mbar_init(aempty + s, CONS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  const int lane = tid & 31;
+  const double2 alpha = make_double2(0.0, -s_k);      // Python complex(-1j * tau / k)
+  const double2 one = make_double2(1.0, 0.0);
+  const double g = -op.gamma;
+  double nrm = 0.0;
+
+  if (tid >= CONS) {
+    const int pl = tid - CONS;
+    if (pl < SPLIT) {
+      // ---------------- producer lanes: stream the partner tiles in row order
+      constexpr unsigned pmask = (SPLIT == 32) ? 0xffffffffu : ((1u << SPLIT) - 1u);
+      constexpr uint32_t part = CHUNK_BYTES / SPLIT;
+      auto issue = [&](uint64_t* fb, double2* dst, const double2* src) {
+        if (pl == 0) mbar_expect_tx(fb, CHUNK_BYTES);
+        __syncwarp(pmask);
+        bulk_g2s(reinterpret_cast<char*>(dst) + pl * part, reinterpret_cast<const char*>(src) + pl * part,
+                 part, fb);
+      };
+      uint32_t it = 0, ti = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
+        const uint32_t H = (uint32_t)tile;
+        const int hs = __popc(H);
+        {   // the tile's acc values, consumed in the epilogue
+          const int ab = ti & 1;
+          mbar_wait(aempty + ab, ((ti >> 1) & 1) ^ 1);
+          issue(afull + ab, accbuf + (size_t)ab * TILE, acc_in + ((int64_t)H << LB));
+        }
+        uint32_t setm = H, clrm = (~H) & hmask;
+        for (int c = 0; c <= nh; ++c) {
+          uint32_t src = H;
+          if (c < hs) {
+            const int b = 31 - __clz(setm);
+            setm ^= 1u << b;
+            src = H ^ (1u << b);
+          } else if (c > hs) {
+            const int b = __ffs(clrm) - 1;
+            clrm ^= 1u << b;
+            src = H ^ (1u << b);
+          }
+          const int s = it % NS;
+          mbar_wait(empty + s, ((it / NS) & 1) ^ 1);
+          issue(full + s, ring + (size_t)s * TILE, tin + ((int64_t)src << LB));
+          ++it;
+        }
+      }
+    } else if (op.bits) {
+      // ---------------- fix-up lanes: marked rows (length dim + 1, the
+      // diagonal -psi[v] between the set and the clear neighbours) of this
+      // CTA's tiles; the consumers leave those vertices alone
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int w = pl - SPLIT; w < TILE / 32; w += 32 - SPLIT) {
+          uint32_t word = __ldg(op.bits + (tile << (LB - 5)) + w);
+          while (word) {
+            const int bit = __ffs(word) - 1;
+            word &= word - 1;
+            const int64_t v = (tile << LB) + w * 32 + bit;
+            const double2 t = cmul_np(alpha, hc_marked_row(dim, g, tin, v));
+            tout[v] = t;
+            acc_out[v] = cadd(acc_in[v], cmul_np(one, t));
+            nrm = __fma_rn(t.x, t.x, __fma_rn(t.y, t.y, nrm));
+          }
+        }
+      }
+    }
+  } else {
+    // ---------------- consumers
+    const int m = dim - 1;
+    const int main_end = m - (m % 4);
+    // the low-segment order of each owned l (same for every tile): nibble q =
+    // the bit flipped by the q-th element (set bits high->low, then clear
+    // bits low->high)
+    uint64_t order[VPT];
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+      const uint32_t l = (uint32_t)(tid + j * CONS);
+      uint32_t sm = l, cm = (~l) & (TILE - 1);
+      const int pc = __popc(l);
+      uint64_t o = 0;
+      for (int q = 0; q < LB; ++q) {
+        int b;
+        if (q < pc) {
+          b = 31 - __clz(sm);
+          sm ^= 1u << b;
+        } else {
+          b = __ffs(cm) - 1;
+          cm ^= 1u << b;
+        }
+        o |= (uint64_t)b << (4 * q);
+      }
+      order[j] = o;
+    }
+    uint32_t it = 0, ti = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
+      const uint32_t H = (uint32_t)tile;
+      const int hs = __popc(H);
+      PosAccs<VPT> acc;
+      acc.init();
+      for (int c = 0; c <= nh; ++c) {
+        const int s = it % NS;
+        mbar_wait(full + s, (it / NS) & 1);
+        const double2* ch = ring + (size_t)s * TILE;
+        double2 e[VPT];
+        if (c == hs) {
+#pragma unroll
+          for (int q = 0; q < LB; ++q) {
+#pragma unroll
+            for (int j = 0; j < VPT; ++j) {
+              const uint32_t b = (uint32_t)(order[j] >> (4 * q)) & 15u;
+              e[j] = scale_real_fin(g, ch[(uint32_t)(tid + j * CONS) ^ (1u << b)]);
+            }
+            acc.push(pos_slot(hs + q, main_end), e);
+          }
+        } else {
+          const int p = (c < hs) ? c : c + LB - 1;
+#pragma unroll
+          for (int j = 0; j < VPT; ++j) e[j] = scale_real_fin(g, ch[tid + j * CONS]);
+          acc.push(pos_slot(p, main_end), e);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
+        ++it;
+      }
+      uint32_t mword[VPT];
+#pragma unroll
+      for (int j = 0; j < VPT; ++j) {
+        const int64_t v = ((int64_t)H << LB) + tid + j * CONS;
+        mword[j] = op.bits ? __ldg(op.bits + (v >> 5)) : 0u;
+      }
+      const int ab = ti & 1;
+      mbar_wait(afull + ab, (ti >> 1) & 1);
+      const double2* ach = accbuf + (size_t)ab * TILE;
+#pragma unroll
+      for (int j = 0; j < VPT; ++j) {
+        const int64_t v = ((int64_t)H << LB) + tid + j * CONS;
+        if ((mword[j] >> (v & 31)) & 1u) continue;   // marked: fix-up lanes
+        const double2 t = cmul_np(alpha, acc.result(j, m, main_end));
+        tout[v] = t;
+        __stcs(acc_out + v, cadd(ach[tid + j * CONS], cmul_np(one, t)));
+        nrm = __fma_rn(t.x, t.x, __fma_rn(t.y, t.y, nrm));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(aempty + ab);
+    }
+  }
+  // deterministic block reduction: consumers + fix-up lanes, fixed order
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nrm = __dadd_rn(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
+  if (lane == 0) red[tid >> 5] = nrm;
+  __syncthreads();
+  if (tid == 0) {
+    double r = 0.0;
+    for (int w = 0; w < CONS / 32 + 1; ++w) r = __dadd_rn(r, red[w]);
+    partial[blockIdx.x] = r;
+  }
+}
+
+// launch one term; returns the number of partials the kernel wrote
+template <int NS, int SPLIT, int CONS>
+void launch_stream(const HcStream& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
+                   const double2* ain, double2* acc, double s_k, const int* flags, double* partial) {
+  static bool configured[256] = {};
+  const int dev = op.device & 255;
+  if (!configured[dev]) {
+    cudaFuncSetAttribute(hc_stream_kernel<NS, SPLIT, CONS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)hcs::smem_bytes(NS));
+    configured[dev] = true;
+  }
+  hc_stream_kernel<NS, SPLIT, CONS><<<op.grid, CONS + 32, hcs::smem_bytes(NS), s>>>(op, n, tin, tout, ain, acc,
+                                                                                    s_k, flags, partial);
+}
+
+int launch_term(const HcStream& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
+                const double2* ain, double2* acc, double s_k, const int* flags, double* partial) {
+  // QWB_HC_STREAM = CONS/256 * 10000 + NS * 100 + SPLIT (tuning knob)
+  switch (op.variant) {
+    case 601: launch_stream<6, 1, 256>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+    case 1001: launch_stream<10, 1, 256>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+    case 20601: launch_stream<6, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+    default: launch_stream<8, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+  }
+  return op.grid;
+}
+
 template <int MAXD>
-void launch_term(const HcPos<MAXD>& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
+int launch_term(const HcPos<MAXD>& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
                  const double2* ain, double2* acc, double s_k, const int* flags, double* partial) {
   hc_pos_kernel<MAXD><<<kTermBlocks, kTermThreads, 0, s>>>(op, n, tin, tout, ain, acc, s_k, flags, partial);
+  return kTermBlocks;
 }
 
 template <class Op>
-void launch_term(const Op& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
+int launch_term(const Op& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
                  const double2* ain, double2* acc, double s_k, const int* flags, double* partial) {
   term_kernel<Op><<<kTermBlocks, kTermThreads, 0, s>>>(op, n, tin, tout, ain, acc, s_k, flags, partial);
+  return kTermBlocks;
 }
 
 template <int MAXD>
-void launch_term(const HcTile<MAXD>& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
+int launch_term(const HcTile<MAXD>& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
                  const double2* ain, double2* acc, double s_k, const int* flags, double* partial) {
   hc_term_kernel<MAXD><<<kTermBlocks, kHcBlock, 0, s>>>(op, n, tin, tout, ain, acc, s_k, flags, partial);
+  return kTermBlocks;
 }
 
 __global__ void apply_kernel_hc(HypercubeOp<32> op, int64_t n, const double2* __restrict__ x,
@@ -436,8 +804,8 @@ int evolve(qwb_ctx* ctx, const Op& op, int64_t n, double2* psi, double2* work, i
         double2* tout = (k % 2) ? ta : tb;
         const double2* ain = (k == 1) ? bufs[cur] : acc;
         const double s_k = tau / (double)k;
-        launch_term(op, s, n, tin, tout, ain, acc, s_k, flags, partial);
-        term_finalize_kernel<<<1, kTermThreads, 0, s>>>(partial, kTermBlocks, floor_, k, flags,
+        const int nparts = launch_term(op, s, n, tin, tout, ain, acc, s_k, flags, partial);
+        term_finalize_kernel<<<1, kTermThreads, 0, s>>>(partial, nparts, floor_, k, flags,
                                                         flags + 1);
       }
       QWB_LAUNCH_CHECK(ctx, "term kernels");
@@ -479,14 +847,26 @@ int qwb_taylor_evolve_hypercube(qwb_ctx* ctx, int dim, double gamma, const uint3
   double2* p = reinterpret_cast<double2*>(psi);
   double2* w = reinterpret_cast<double2*>(work);
   cudaStream_t s = qwb::as_stream(stream);
-  // QWB_HC_KERNEL: 2 = positional (default), 1 = subcube tile, 0 = generic gather
+  // QWB_HC_KERNEL: 3 = TMA-streamed tiles (default), 2 = positional gather,
+  // 1 = subcube tile, 0 = generic gather
   static int tiled = -1;
   if (tiled < 0) {
     const char* e = getenv("QWB_HC_KERNEL");
-    tiled = (e && *e) ? atoi(e) : 2;
+    tiled = (e && *e) ? atoi(e) : 3;
   }
   if (dim <= 8) {
     HypercubeOp<8> op{dim, gamma, marked_bits};
+    return evolve(ctx, op, n, p, w, substeps, tau, floor, max_terms, terms_host, s);
+  }
+  if (tiled == 3 && dim >= hcs::LB) {
+    static int variant = -1;
+    if (variant < 0) {
+      const char* e = getenv("QWB_HC_STREAM");
+      variant = (e && *e) ? atoi(e) : 20801;
+    }
+    const int64_t ntiles = n >> hcs::LB;
+    HcStream op{dim, gamma, marked_bits, (int)(ntiles < ctx->num_sms ? ntiles : ctx->num_sms), ctx->device,
+                variant};
     return evolve(ctx, op, n, p, w, substeps, tau, floor, max_terms, terms_host, s);
   }
   if (tiled == 2 && dim >= 10) {
