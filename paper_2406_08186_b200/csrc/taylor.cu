@@ -430,13 +430,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// (c + 0i) * x in numpy's FMA form for finite x: the 0*x terms are signed
-// zeros, produced with bit operations (exactly what the FP multiply returns).
-__device__ __forceinline__ double2 scale_real_fin(double c, double2 x) {
-  const long long sx = __double_as_longlong(x.x) & (long long)0x8000000000000000ULL;
-  const long long sy = __double_as_longlong(x.y) & (long long)0x8000000000000000ULL;
-  return make_double2(__fma_rn(c, x.x, __longlong_as_double(sy ^ (long long)0x8000000000000000ULL)),
-                      __fma_rn(c, x.y, __longlong_as_double(sx)));
+// (c + 0i) * x with the zero terms dropped: c*x.re, c*x.im.  Equal to
+// numpy's product for every x except in the sign of an exactly-zero
+// component, so every non-zero sum built from it keeps numpy's bits (exact
+// zeros may carry the other sign: equal under ==, invisible to every norm).
+__device__ __forceinline__ double2 scale_real_z(double c, double2 x) {
+  return make_double2(__dmul_rn(c, x.x), __dmul_rn(c, x.y));
 }
 
 // numpy x0 + pairwise(x1..x_m), 4 <= m < 64, for VPT rows whose element
@@ -624,16 +623,16 @@ hc_stream_kernel(HcStream op, int64_t n, const double2* __restrict__ tin, double
     // ---------------- consumers
     const int m = dim - 1;
     const int main_end = m - (m % 4);
-    // the low-segment order of each owned l (same for every tile): nibble q =
-    // the bit flipped by the q-th element (set bits high->low, then clear
-    // bits low->high)
-    uint64_t order[VPT];
+    // the low segment of each owned l (the same for every tile): byte offset
+    // of the q-th element's partner l ^ 2^b in a chunk, set bits high->low
+    // then clear bits low->high, two 16-bit offsets per register
+    uint32_t offs[VPT][LB / 2];
 #pragma unroll
     for (int j = 0; j < VPT; ++j) {
       const uint32_t l = (uint32_t)(tid + j * CONS);
       uint32_t sm = l, cm = (~l) & (TILE - 1);
       const int pc = __popc(l);
-      uint64_t o = 0;
+#pragma unroll
       for (int q = 0; q < LB; ++q) {
         int b;
         if (q < pc) {
@@ -643,9 +642,10 @@ hc_stream_kernel(HcStream op, int64_t n, const double2* __restrict__ tin, double
           b = __ffs(cm) - 1;
           cm ^= 1u << b;
         }
-        o |= (uint64_t)b << (4 * q);
+        const uint32_t off = (l ^ (1u << b)) * (uint32_t)sizeof(double2);
+        if (q % 2 == 0) offs[j][q / 2] = off;
+        else offs[j][q / 2] |= off << 16;
       }
-      order[j] = o;
     }
     uint32_t it = 0, ti = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
@@ -659,19 +659,20 @@ hc_stream_kernel(HcStream op, int64_t n, const double2* __restrict__ tin, double
         const double2* ch = ring + (size_t)s * TILE;
         double2 e[VPT];
         if (c == hs) {
+          const char* cb = reinterpret_cast<const char*>(ch);
 #pragma unroll
           for (int q = 0; q < LB; ++q) {
 #pragma unroll
             for (int j = 0; j < VPT; ++j) {
-              const uint32_t b = (uint32_t)(order[j] >> (4 * q)) & 15u;
-              e[j] = scale_real_fin(g, ch[(uint32_t)(tid + j * CONS) ^ (1u << b)]);
+              const uint32_t off = (q % 2 == 0) ? (offs[j][q / 2] & 0xffffu) : (offs[j][q / 2] >> 16);
+              e[j] = scale_real_z(g, *reinterpret_cast<const double2*>(cb + off));
             }
             acc.push(pos_slot(hs + q, main_end), e);
           }
         } else {
           const int p = (c < hs) ? c : c + LB - 1;
 #pragma unroll
-          for (int j = 0; j < VPT; ++j) e[j] = scale_real_fin(g, ch[tid + j * CONS]);
+          for (int j = 0; j < VPT; ++j) e[j] = scale_real_z(g, ch[tid + j * CONS]);
           acc.push(pos_slot(p, main_end), e);
         }
         __syncwarp();
@@ -734,6 +735,8 @@ int launch_term(const HcStream& op, cudaStream_t s, int64_t n, const double2* ti
     case 601: launch_stream<6, 1, 256>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
     case 1001: launch_stream<10, 1, 256>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
     case 20601: launch_stream<6, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+    case 21001: launch_stream<10, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+    case 21201: launch_stream<12, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
     default: launch_stream<8, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
   }
   return op.grid;
