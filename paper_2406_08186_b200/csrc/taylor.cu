@@ -22,6 +22,8 @@
 // hypercube H = -gamma A - sum_M |v><v| whose row v lists, in ascending column
 // order, v with its set bits cleared high->low, the diagonal (if v marked),
 // then v with its clear bits set low->high.
+#include <type_traits>
+
 #include "qwb_internal.cuh"
 
 namespace {
@@ -422,6 +424,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_wait_u32(uint32_t addr, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "HCS_WAITU_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra HCS_WAITU_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t addr) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(addr) : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
@@ -437,64 +453,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ double2 scale_real_z(double c, double2 x) {
   return make_double2(__dmul_rn(c, x.x), __dmul_rn(c, x.y));
 }
-
-// numpy x0 + pairwise(x1..x_m), 4 <= m < 64, for VPT rows whose element
-// positions agree (warp-uniform slot): x0, then accumulators c0..c3 take
-// elements 1 + 4q + j, the tail (elements after main_end) is added to the
-// combined (c0 + c1) + (c2 + c3).  Accumulators start at -0.0, so the first
-// addition returns the element itself bit for bit (signed zeros included).
-// slot: 0 = x0, 1..4 = c0..c3, 5 = first tail element, 6 = later tail.
-__device__ __forceinline__ int pos_slot(int p, int main_end) {
-  if (p == 0) return 0;
-  const int i = p - 1;
-  if (i < main_end) return 1 + (i & 3);
-  return i == main_end ? 5 : 6;
-}
-
-template <int V>
-struct PosAccs {
-  double2 x0[V], c0[V], c1[V], c2[V], c3[V];
-  __device__ __forceinline__ void init() {
-#pragma unroll
-    for (int j = 0; j < V; ++j) x0[j] = c0[j] = c1[j] = c2[j] = c3[j] = make_double2(-0.0, -0.0);
-  }
-  __device__ __forceinline__ void push(int slot, const double2 (&e)[V]) {
-    switch (slot) {
-      case 0:
-#pragma unroll
-        for (int j = 0; j < V; ++j) x0[j] = cadd(x0[j], e[j]);
-        break;
-      case 1:
-#pragma unroll
-        for (int j = 0; j < V; ++j) c0[j] = cadd(c0[j], e[j]);
-        break;
-      case 2:
-#pragma unroll
-        for (int j = 0; j < V; ++j) c1[j] = cadd(c1[j], e[j]);
-        break;
-      case 3:
-#pragma unroll
-        for (int j = 0; j < V; ++j) c2[j] = cadd(c2[j], e[j]);
-        break;
-      case 4:
-#pragma unroll
-        for (int j = 0; j < V; ++j) c3[j] = cadd(c3[j], e[j]);
-        break;
-      case 5:
-#pragma unroll
-        for (int j = 0; j < V; ++j) c0[j] = cadd(cadd(cadd(c0[j], c1[j]), cadd(c2[j], c3[j])), e[j]);
-        break;
-      default:
-#pragma unroll
-        for (int j = 0; j < V; ++j) c0[j] = cadd(c0[j], e[j]);
-        break;
-    }
-  }
-  __device__ __forceinline__ double2 result(int j, int m, int main_end) const {
-    const double2 r = (m == main_end) ? cadd(cadd(c0[j], c1[j]), cadd(c2[j], c3[j])) : c0[j];
-    return cadd(x0[j], r);
-  }
-};
 
 // marked row v: -1 * psi[v] sits between the set and the clear neighbours
 // (row length dim + 1); out of line so the streaming loop keeps its registers
@@ -647,37 +605,98 @@ hc_stream_kernel(HcStream op, int64_t n, const double2* __restrict__ tin, double
         else offs[j][q / 2] |= off << 16;
       }
     }
-    uint32_t it = 0, ti = 0;
+    // Accumulators of numpy's x0 + pairwise(x1..x_m): x0, ac[0..3] take the
+    // elements at row positions 1 + 4k + a, the tail (positions past
+    // main_end) is added to the combined (ac0 + ac1) + (ac2 + ac3) in ac[0].
+    // A chunk's slot depends only on its index modulo 4 (set partner c at
+    // position c, clear partner c at position c + LB - 1), so the chunk loop
+    // is unrolled by 4 and every slot is a compile-time register; the own
+    // tile's ten positions start at hs, one of four compile-time rotations.
+    const uint32_t full_u32 = smem_u32(full), empty_u32 = smem_u32(empty);
+    uint32_t s = 0, ph = 0, ti = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
       const uint32_t H = (uint32_t)tile;
       const int hs = __popc(H);
-      PosAccs<VPT> acc;
-      acc.init();
-      for (int c = 0; c <= nh; ++c) {
-        const int s = it % NS;
-        mbar_wait(full + s, (it / NS) & 1);
-        const double2* ch = ring + (size_t)s * TILE;
-        double2 e[VPT];
-        if (c == hs) {
-          const char* cb = reinterpret_cast<const char*>(ch);
+      double2 x0[VPT], ac[4][VPT];
 #pragma unroll
-          for (int q = 0; q < LB; ++q) {
+      for (int j = 0; j < VPT; ++j) x0[j] = ac[0][j] = ac[1][j] = ac[2][j] = ac[3][j] = make_double2(-0.0, -0.0);
+      auto add_tail = [&](int i, const double2 (&e)[VPT]) {
 #pragma unroll
-            for (int j = 0; j < VPT; ++j) {
-              const uint32_t off = (q % 2 == 0) ? (offs[j][q / 2] & 0xffffu) : (offs[j][q / 2] >> 16);
-              e[j] = scale_real_z(g, *reinterpret_cast<const double2*>(cb + off));
-            }
-            acc.push(pos_slot(hs + q, main_end), e);
-          }
-        } else {
-          const int p = (c < hs) ? c : c + LB - 1;
-#pragma unroll
-          for (int j = 0; j < VPT; ++j) e[j] = scale_real_z(g, ch[tid + j * CONS]);
-          acc.push(pos_slot(p, main_end), e);
+        for (int j = 0; j < VPT; ++j) {
+          if (i == main_end) ac[0][j] = cadd(cadd(ac[0][j], ac[1][j]), cadd(ac[2][j], ac[3][j]));
+          ac[0][j] = cadd(ac[0][j], e[j]);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty + s);
-        ++it;
+      };
+      auto fold_own = [&](const double2* ch, auto Rc) {   // positions hs .. hs + LB - 1
+        constexpr int R = decltype(Rc)::value;           // hs & 3
+        const char* cb = reinterpret_cast<const char*>(ch);
+#pragma unroll
+        for (int q = 0; q < LB; ++q) {
+          double2 e[VPT];
+#pragma unroll
+          for (int j = 0; j < VPT; ++j) {
+            const uint32_t off = (q % 2 == 0) ? (offs[j][q / 2] & 0xffffu) : (offs[j][q / 2] >> 16);
+            e[j] = scale_real_z(g, *reinterpret_cast<const double2*>(cb + off));
+          }
+          const int i = hs + q - 1;
+          if (i < 0) {
+#pragma unroll
+            for (int j = 0; j < VPT; ++j) x0[j] = cadd(x0[j], e[j]);
+          } else if (i < main_end) {
+            const int a = (R + q + 3) & 3;
+#pragma unroll
+            for (int j = 0; j < VPT; ++j) ac[a][j] = cadd(ac[a][j], e[j]);
+          } else {
+            add_tail(i, e);
+          }
+        }
+      };
+      for (int c0 = 0; c0 <= nh; c0 += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + u;
+          if (c <= nh) {
+            mbar_wait_u32(full_u32 + 8 * s, ph);
+            const double2* ch = ring + (size_t)s * TILE;
+            if (c == hs) {
+              switch (hs & 3) {
+                case 0: fold_own(ch, std::integral_constant<int, 0>{}); break;
+                case 1: fold_own(ch, std::integral_constant<int, 1>{}); break;
+                case 2: fold_own(ch, std::integral_constant<int, 2>{}); break;
+                default: fold_own(ch, std::integral_constant<int, 3>{}); break;
+              }
+            } else {
+              double2 e[VPT];
+#pragma unroll
+              for (int j = 0; j < VPT; ++j) e[j] = scale_real_z(g, ch[tid + j * CONS]);
+              if (c < hs) {            // set partner, position c
+                if (c == 0) {
+#pragma unroll
+                  for (int j = 0; j < VPT; ++j) x0[j] = cadd(x0[j], e[j]);
+                } else {
+                  const int a = (u + 3) & 3;
+#pragma unroll
+                  for (int j = 0; j < VPT; ++j) ac[a][j] = cadd(ac[a][j], e[j]);
+                }
+              } else {                 // clear partner, position c + LB - 1
+                const int i = c + LB - 2;
+                if (i < main_end) {
+                  const int a = (u + LB - 2) & 3;
+#pragma unroll
+                  for (int j = 0; j < VPT; ++j) ac[a][j] = cadd(ac[a][j], e[j]);
+                } else {
+                  add_tail(i, e);
+                }
+              }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive_u32(empty_u32 + 8 * s);
+            if (++s == NS) {
+              s = 0;
+              ph ^= 1u;
+            }
+          }
+        }
       }
       uint32_t mword[VPT];
 #pragma unroll
@@ -692,7 +711,8 @@ hc_stream_kernel(HcStream op, int64_t n, const double2* __restrict__ tin, double
       for (int j = 0; j < VPT; ++j) {
         const int64_t v = ((int64_t)H << LB) + tid + j * CONS;
         if ((mword[j] >> (v & 31)) & 1u) continue;   // marked: fix-up lanes
-        const double2 t = cmul_np(alpha, acc.result(j, m, main_end));
+        const double2 r = (m == main_end) ? cadd(cadd(ac[0][j], ac[1][j]), cadd(ac[2][j], ac[3][j])) : ac[0][j];
+        const double2 t = cmul_np(alpha, cadd(x0[j], r));
         tout[v] = t;
         __stcs(acc_out + v, cadd(ach[tid + j * CONS], cmul_np(one, t)));
         nrm = __fma_rn(t.x, t.x, __fma_rn(t.y, t.y, nrm));
