@@ -227,6 +227,26 @@ int qwb_taylor_evolve_csr(qwb_ctx* ctx, int64_t n, const int64_t* row_offsets, c
 int qwb_taylor_evolve_hypercube(qwb_ctx* ctx, int dim, double gamma, const uint32_t* marked_bits,
                                 qwb_z* psi, qwb_z* work, int64_t substeps, double tau, double floor,
                                 int max_terms, int* terms_host, void* stream);
+/* Sharded matrix-free hypercube evolve (no reference counterpart; SURVEY
+ * §8(e) C4): 2^log2_shards ranks, rank r (ctx->rank, NCCL communicator from
+ * qwb_comm_init, ctx->nranks == 2^log2_shards) owns the 2^(dim-log2_shards)
+ * consecutive vertices whose top log2_shards bits equal r (psi: its local
+ * slice).  Per Taylor term the term slice is exchanged with the log2_shards
+ * partners r ^ 2^j (NCCL grouped send/recv) and the stop test uses the norm
+ * all-gathered over ranks and summed in rank order, so every rank takes the
+ * same decision and the state is bitwise the single-GPU one.  marked_bits is
+ * the GLOBAL bitmap; floor = tol * ||psi_in|| over the whole state.
+ * work: (3 + log2_shards) * 2^(dim-log2_shards) qwb_z.  dim - log2_shards >= 10. */
+int qwb_taylor_evolve_hypercube_sharded(qwb_ctx* ctx, int dim, int log2_shards, double gamma,
+                                        const uint32_t* marked_bits, qwb_z* psi, qwb_z* work, int64_t substeps,
+                                        double tau, double floor, int max_terms, int* terms_host, void* stream);
+/* the same decomposition with all 2^log2_shards shards on ONE device (the
+ * partner slices are read in place instead of exchanged): psi_host / work_host
+ * are host arrays of per-shard device pointers (work: 3 * 2^(dim-log2_shards)). */
+int qwb_taylor_evolve_hypercube_shards_local(qwb_ctx* ctx, int dim, int log2_shards, double gamma,
+                                             const uint32_t* marked_bits, qwb_z* const* psi_host,
+                                             qwb_z* const* work_host, int64_t substeps, double tau, double floor,
+                                             int max_terms, int* terms_host, void* stream);
 /* one matrix-free hypercube H x (for tests / backend parity). */
 int qwb_hypercube_apply(qwb_ctx* ctx, int dim, double gamma, const uint32_t* marked_bits,
                         const qwb_z* x, qwb_z* y, void* stream);

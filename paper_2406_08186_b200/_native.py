@@ -90,6 +90,10 @@ SIGNATURES = {
     "qwb_norm": [_vp, _i64, _vp, _p_dbl, _vp],
     "qwb_check_finite": [_vp, _i64, _vp, _p_int, _vp],
     "qwb_taylor_evolve_csr": [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _dbl, _dbl, _i32, _p_int, _vp],
+    "qwb_taylor_evolve_hypercube_sharded": [_vp, _i32, _i32, _dbl, _vp, _vp, _vp, _i64, _dbl, _dbl, _i32,
+                                            _p_int, _vp],
+    "qwb_taylor_evolve_hypercube_shards_local": [_vp, _i32, _i32, _dbl, _vp, C.POINTER(_vp), C.POINTER(_vp),
+                                                 _i64, _dbl, _dbl, _i32, _p_int, _vp],
     "qwb_taylor_evolve_hypercube": [_vp, _i32, _dbl, _vp, _vp, _vp, _i64, _dbl, _dbl, _i32, _p_int,
                                     _vp],
     "qwb_hypercube_apply": [_vp, _i32, _dbl, _vp, _vp, _vp, _vp],

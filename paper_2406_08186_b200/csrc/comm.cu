@@ -35,6 +35,7 @@ typedef int (*fn_destroy)(NcclComm);
 typedef int (*fn_sendrecv)(void*, size_t, int, int, NcclComm, cudaStream_t);
 typedef int (*fn_group)(void);
 typedef const char* (*fn_errstr)(int);
+typedef int (*fn_allgather)(const void*, void*, size_t, int, NcclComm, cudaStream_t);
 
 constexpr int kNcclFloat64 = 8;
 
@@ -48,6 +49,7 @@ struct Nccl {
   fn_group group_start = nullptr;
   fn_group group_end = nullptr;
   fn_errstr errstr = nullptr;
+  fn_allgather allgather = nullptr;
 };
 
 Nccl g_nccl;
@@ -68,8 +70,9 @@ int load_nccl(qwb_ctx* ctx) {
   n.group_start = (fn_group)dlsym(h, "ncclGroupStart");
   n.group_end = (fn_group)dlsym(h, "ncclGroupEnd");
   n.errstr = (fn_errstr)dlsym(h, "ncclGetErrorString");
+  n.allgather = (fn_allgather)dlsym(h, "ncclAllGather");
   if (!n.get_uid || !n.init_rank || !n.destroy || !n.send || !n.recv || !n.group_start ||
-      !n.group_end || !n.errstr)
+      !n.group_end || !n.errstr || !n.allgather)
     QWB_FAIL(ctx, QWB_E_NCCL, "NCCL library lacks a required symbol");
   g_nccl = n;
   return QWB_OK;
@@ -83,6 +86,32 @@ int load_nccl(qwb_ctx* ctx) {
   } while (0)
 
 }  // namespace
+
+namespace qwb {
+
+// One grouped exchange: send `send` (count float64s) to every peer and receive
+// each peer's buffer into recv[i], on stream s.
+int nccl_exchange(qwb_ctx* ctx, const void* send, void* const* recv, const int* peers, int npeers,
+                  size_t count, cudaStream_t s) {
+  if (!ctx->comm) QWB_FAIL(ctx, QWB_E_NCCL, "qwb_comm_init has not been called");
+  NcclComm comm = (NcclComm)ctx->comm;
+  QWB_NCCL(ctx, g_nccl.group_start());
+  for (int i = 0; i < npeers; ++i) {
+    QWB_NCCL(ctx, g_nccl.send(const_cast<void*>(send), count, kNcclFloat64, peers[i], comm, s));
+    QWB_NCCL(ctx, g_nccl.recv(recv[i], count, kNcclFloat64, peers[i], comm, s));
+  }
+  QWB_NCCL(ctx, g_nccl.group_end());
+  return QWB_OK;
+}
+
+// recv[r * count ...] = rank r's send (count float64s), on stream s
+int nccl_allgather_f64(qwb_ctx* ctx, const double* send, double* recv, size_t count, cudaStream_t s) {
+  if (!ctx->comm) QWB_FAIL(ctx, QWB_E_NCCL, "qwb_comm_init has not been called");
+  QWB_NCCL(ctx, g_nccl.allgather(send, recv, count, kNcclFloat64, (NcclComm)ctx->comm, s));
+  return QWB_OK;
+}
+
+}  // namespace qwb
 
 extern "C" {
 

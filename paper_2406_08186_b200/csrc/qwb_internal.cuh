@@ -33,6 +33,10 @@ int cuda_status(qwb_ctx* ctx, cudaError_t e, const char* what);
 // scratch of at least `bytes` (256-B aligned), stream-ordered
 int workspace(qwb_ctx* ctx, size_t bytes, cudaStream_t s, void** out);
 int begin(qwb_ctx* ctx);   // checks ctx alive and sets the device
+// NCCL (comm.cu): grouped send/recv with each peer; float64 all-gather
+int nccl_exchange(qwb_ctx* ctx, const void* send, void* const* recv, const int* peers, int npeers,
+                  size_t count, cudaStream_t s);
+int nccl_allgather_f64(qwb_ctx* ctx, const double* send, double* recv, size_t count, cudaStream_t s);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

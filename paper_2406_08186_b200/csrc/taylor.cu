@@ -454,34 +454,52 @@ __device__ __forceinline__ double2 scale_real_z(double c, double2 x) {
   return make_double2(__dmul_rn(c, x.x), __dmul_rn(c, x.y));
 }
 
-// marked row v: -1 * psi[v] sits between the set and the clear neighbours
-// (row length dim + 1); out of line so the streaming loop keeps its registers
-__device__ __noinline__ double2 hc_marked_row(int dim, double g, const double2* __restrict__ tin, int64_t v) {
-  StreamRow sr;
-  sr.init(dim + 1);
-  const double2 gg = make_double2(g, 0.0);
-  for (int b = dim - 1; b >= 0; --b)
-    if ((v >> b) & 1) sr.push(cmul_np(gg, __ldg(tin + (v ^ (1LL << b)))));
-  sr.push(cmul_np(make_double2(-1.0, 0.0), __ldg(tin + v)));
-  for (int b = 0; b < dim; ++b)
-    if (!((v >> b) & 1)) sr.push(cmul_np(gg, __ldg(tin + (v ^ (1LL << b)))));
-  return sr.result();
-}
+constexpr int kMaxShardBits = 5;   // up to 32 shards
 
+// n below is the LOCAL vertex count 2^dim_loc; a shard holds the vertices
+// whose top dim - dim_loc bits equal its rank (single GPU: dim_loc = dim).
 struct HcStream {
-  int dim;
+  int dim;        // global hypercube dimension
+  int dim_loc;    // log2 of the vertices this launch owns
+  int rank;       // shard index (top bits of every owned vertex)
   double gamma;
-  const uint32_t* __restrict__ bits;
+  const uint32_t* __restrict__ bits;   // GLOBAL marked bitmap (or null)
   int grid;
   int device;
   int variant;
+  // term_{k-1} of the partner shard across each rank bit (rank ^ 2^j), same
+  // local indexing as tin: received by NCCL, or the partner's own buffer
+  const double2* remote[kMaxShardBits];
 };
+using HcStreamArgs = HcStream;
+
+// marked row v: -1 * psi[v] sits between the set and the clear neighbours
+// (row length dim + 1); out of line so the streaming loop keeps its registers.
+// vl: local index, vg: global vertex id; neighbours across rank bits come
+// from the partner shards' term buffers.
+__device__ __noinline__ double2 hc_marked_row(const HcStreamArgs& a, double g, const double2* __restrict__ tin,
+                                              int64_t vl, int64_t vg) {
+  auto fetch = [&](int b) {
+    return b < a.dim_loc ? __ldg(tin + (vl ^ (1LL << b))) : __ldg(a.remote[b - a.dim_loc] + vl);
+  };
+  StreamRow sr;
+  sr.init(a.dim + 1);
+  const double2 gg = make_double2(g, 0.0);
+  for (int b = a.dim - 1; b >= 0; --b)
+    if ((vg >> b) & 1) sr.push(cmul_np(gg, fetch(b)));
+  sr.push(cmul_np(make_double2(-1.0, 0.0), __ldg(tin + vl)));
+  for (int b = 0; b < a.dim; ++b)
+    if (!((vg >> b) & 1)) sr.push(cmul_np(gg, fetch(b)));
+  return sr.result();
+}
+
+
 
 // NS: ring stages; SPLIT: producer lanes, each copying 1/SPLIT of a chunk;
 // CONS: consumer threads (+ one producer warp), TILE / CONS vertices each
 template <int NS, int SPLIT, int CONS>
 __global__ void __launch_bounds__(CONS + 32, 1)
-hc_stream_kernel(HcStream op, int64_t n, const double2* __restrict__ tin, double2* __restrict__ tout,
+hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* __restrict__ tin, double2* __restrict__ tout,
                  const double2* acc_in, double2* acc_out, double s_k, const int* __restrict__ done,
                  double* __restrict__ partial) {
   using namespace hcs;
@@ -497,8 +515,11 @@ hc_stream_kernel(HcStream op, int64_t n, const double2* __restrict__ tin, double
   __shared__ double red[CONS / 32 + 1];
   const int tid = threadIdx.x;
   const int dim = op.dim;
-  const int nh = dim - LB;                            // high bits
+  const int nh = dim - LB;                            // high bits (global)
+  const int nh_loc = op.dim_loc - LB;                 // high bits inside the shard
   const uint32_t hmask = (nh >= 32) ? 0xffffffffu : ((1u << nh) - 1u);
+  const uint32_t hbase = (uint32_t)op.rank << nh_loc;   // rank bits of every tile index
+  const int64_t vbase = (int64_t)op.rank << op.dim_loc;
   const int64_t ntiles = n >> LB;
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -533,28 +554,29 @@ hc_stream_kernel(HcStream op, int64_t n, const double2* __restrict__ tin, double
       };
       uint32_t it = 0, ti = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
-        const uint32_t H = (uint32_t)tile;
+        const uint32_t Hl = (uint32_t)tile, H = hbase | Hl;
         const int hs = __popc(H);
         {   // the tile's acc values, consumed in the epilogue
           const int ab = ti & 1;
           mbar_wait(aempty + ab, ((ti >> 1) & 1) ^ 1);
-          issue(afull + ab, accbuf + (size_t)ab * TILE, acc_in + ((int64_t)H << LB));
+          issue(afull + ab, accbuf + (size_t)ab * TILE, acc_in + ((int64_t)Hl << LB));
         }
         uint32_t setm = H, clrm = (~H) & hmask;
         for (int c = 0; c <= nh; ++c) {
-          uint32_t src = H;
+          int b = -1;   // partner across high bit b (-1: the tile itself)
           if (c < hs) {
-            const int b = 31 - __clz(setm);
+            b = 31 - __clz(setm);
             setm ^= 1u << b;
-            src = H ^ (1u << b);
           } else if (c > hs) {
-            const int b = __ffs(clrm) - 1;
+            b = __ffs(clrm) - 1;
             clrm ^= 1u << b;
-            src = H ^ (1u << b);
           }
+          const double2* src = b < 0 ? tin + ((int64_t)Hl << LB)
+                               : b < nh_loc ? tin + ((int64_t)(Hl ^ (1u << b)) << LB)
+                                            : op.remote[b - nh_loc] + ((int64_t)Hl << LB);
           const int s = it % NS;
           mbar_wait(empty + s, ((it / NS) & 1) ^ 1);
-          issue(full + s, ring + (size_t)s * TILE, tin + ((int64_t)src << LB));
+          issue(full + s, ring + (size_t)s * TILE, src);
           ++it;
         }
       }
@@ -564,12 +586,12 @@ hc_stream_kernel(HcStream op, int64_t n, const double2* __restrict__ tin, double
       // CTA's tiles; the consumers leave those vertices alone
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         for (int w = pl - SPLIT; w < TILE / 32; w += 32 - SPLIT) {
-          uint32_t word = __ldg(op.bits + (tile << (LB - 5)) + w);
+          uint32_t word = __ldg(op.bits + ((vbase + (tile << LB)) >> 5) + w);
           while (word) {
             const int bit = __ffs(word) - 1;
             word &= word - 1;
             const int64_t v = (tile << LB) + w * 32 + bit;
-            const double2 t = cmul_np(alpha, hc_marked_row(dim, g, tin, v));
+            const double2 t = cmul_np(alpha, hc_marked_row(op, g, tin, v, vbase + v));
             tout[v] = t;
             acc_out[v] = cadd(acc_in[v], cmul_np(one, t));
             nrm = __fma_rn(t.x, t.x, __fma_rn(t.y, t.y, nrm));
@@ -615,7 +637,7 @@ hc_stream_kernel(HcStream op, int64_t n, const double2* __restrict__ tin, double
     const uint32_t full_u32 = smem_u32(full), empty_u32 = smem_u32(empty);
     uint32_t s = 0, ph = 0, ti = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
-      const uint32_t H = (uint32_t)tile;
+      const uint32_t H = hbase | (uint32_t)tile;   // global tile index: row order
       const int hs = __popc(H);
       double2 x0[VPT], ac[4][VPT];
 #pragma unroll
@@ -701,7 +723,7 @@ hc_stream_kernel(HcStream op, int64_t n, const double2* __restrict__ tin, double
       uint32_t mword[VPT];
 #pragma unroll
       for (int j = 0; j < VPT; ++j) {
-        const int64_t v = ((int64_t)H << LB) + tid + j * CONS;
+        const int64_t v = ((int64_t)H << LB) + tid + j * CONS;   // global id
         mword[j] = op.bits ? __ldg(op.bits + (v >> 5)) : 0u;
       }
       const int ab = ti & 1;
@@ -709,7 +731,7 @@ hc_stream_kernel(HcStream op, int64_t n, const double2* __restrict__ tin, double
       const double2* ach = accbuf + (size_t)ab * TILE;
 #pragma unroll
       for (int j = 0; j < VPT; ++j) {
-        const int64_t v = ((int64_t)H << LB) + tid + j * CONS;
+        const int64_t v = (tile << LB) + tid + j * CONS;            // local index
         if ((mword[j] >> (v & 31)) & 1u) continue;   // marked: fix-up lanes
         const double2 r = (m == main_end) ? cadd(cadd(ac[0][j], ac[1][j]), cadd(ac[2][j], ac[3][j])) : ac[0][j];
         const double2 t = cmul_np(alpha, cadd(x0[j], r));
@@ -847,9 +869,207 @@ int evolve(qwb_ctx* ctx, const Op& op, int64_t n, double2* psi, double2* work, i
   return QWB_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Sharded hypercube evolve.  2^S shards of 2^(dim-S) consecutive vertices
+// (shard r = the vertices whose top S bits are r).  Per Taylor term every
+// shard needs, for each rank bit j, the partner shard r ^ 2^j's whole term
+// slice (same local index), so the term loop is:
+//   exchange: NCCL grouped send/recv of term_{k-1} with the S partners
+//             (emulation: the partner's buffer is read in place)
+//   term:     hc_stream_kernel on the local slice, partner tiles across rank
+//             bits streamed from the received slices
+//   norm:     local partial sums -> one float64 per shard -> all-gather ->
+//             every shard sums the 2^S values in rank order (identical stop
+//             decision everywhere)
+// Every vertex's row is computed with the single-GPU formula and order, so
+// states are bitwise equal to one GPU; only the norm's summation tree differs.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kTermThreads)
+term_local_sum_kernel(const double* __restrict__ partial, int nparts, const int* __restrict__ done,
+                      double* __restrict__ out) {
+  if (*done) return;
+  __shared__ double sh[kTermThreads];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) acc = __dadd_rn(acc, partial[i]);
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = kTermThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+__global__ void term_global_finalize_kernel(const double* __restrict__ gsum, int nshards, double floor_, int k,
+                                            int* __restrict__ done, int* __restrict__ terms) {
+  if (*done || threadIdx.x != 0) return;
+  double acc = 0.0;
+  for (int i = 0; i < nshards; ++i) acc = __dadd_rn(acc, gsum[i]);
+  if (__dsqrt_rn(acc) <= floor_) {
+    *done = 1;
+    *terms = k;
+  }
+}
+
+struct ShardSet {
+  int nlocal;                 // shards held by this process (1 with NCCL, 2^S emulated)
+  int first_rank;             // rank of local shard 0
+  bool nccl;
+  double2* bufs[32][4];       // per local shard: psi, work, work + n, work + 2n
+  double2* recv[kMaxShardBits];   // NCCL mode: received partner slices
+};
+
+int evolve_hc_sharded(qwb_ctx* ctx, const HcStream& base, int S, ShardSet& sh, int64_t substeps, double tau,
+                      double floor_, int max_terms, int* terms_host, cudaStream_t s) {
+  if (substeps < 1) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "substeps must be >= 1");
+  if (max_terms < 1) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "max_terms must be >= 1");
+  const int P = 1 << S;
+  const int64_t nloc = 1LL << base.dim_loc;
+  const int grid = base.grid;
+  void* ws;
+  const size_t part_bytes = (size_t)sh.nlocal * grid * sizeof(double);
+  int st = qwb::workspace(ctx, part_bytes + P * sizeof(double) + 256, s, &ws);
+  if (st) return st;
+  double* partial = reinterpret_cast<double*>(ws);
+  double* gsum = partial + (size_t)sh.nlocal * grid;
+  int* flags = reinterpret_cast<int*>(gsum + P);
+  int* pin = reinterpret_cast<int*>(ctx->pinned);
+  int peers[kMaxShardBits];
+  for (int j = 0; j < S; ++j) peers[j] = sh.first_rank ^ (1 << j);
+  int cur = 0;
+  int prev_terms = 8;
+  for (int64_t sub = 0; sub < substeps; ++sub) {
+    int others[3], jj = 0;
+    for (int b = 0; b < 4; ++b)
+      if (b != cur) others[jj++] = b;
+    QWB_CUDA(ctx, cudaMemsetAsync(flags, 0, 2 * sizeof(int), s));
+    int launched = 0;
+    int chunk = prev_terms + 1;
+    bool done = false;
+    while (!done) {
+      if (launched >= max_terms) {
+        QWB_FAIL(ctx, QWB_E_SERIES_NOT_CONVERGED,
+                 "series did not reach the tolerance within %d terms per sub-step", max_terms);
+      }
+      const int upto = launched + chunk < max_terms ? launched + chunk : max_terms;
+      for (int k = launched + 1; k <= upto; ++k) {
+        // buffer roles, identical on every shard
+        const int i_tin = (k == 1) ? cur : ((k % 2) ? others[2] : others[1]);
+        const int i_tout = (k % 2) ? others[1] : others[2];
+        const int i_ain = (k == 1) ? cur : others[0];
+        const int i_acc = others[0];
+        const double s_k = tau / (double)k;
+        if (sh.nccl) {
+          void* rv[kMaxShardBits];
+          for (int j = 0; j < S; ++j) rv[j] = sh.recv[j];
+          st = qwb::nccl_exchange(ctx, sh.bufs[0][i_tin], rv, peers, S, 2 * (size_t)nloc, s);
+          if (st) return st;
+        }
+        for (int i = 0; i < sh.nlocal; ++i) {
+          HcStream op = base;
+          op.rank = sh.first_rank + i;
+          for (int j = 0; j < S; ++j)
+            op.remote[j] = sh.nccl ? sh.recv[j] : sh.bufs[i ^ (1 << j)][i_tin];
+          launch_term(op, s, nloc, sh.bufs[i][i_tin], sh.bufs[i][i_tout], sh.bufs[i][i_ain], sh.bufs[i][i_acc],
+                      s_k, flags, partial + (size_t)i * grid);
+          term_local_sum_kernel<<<1, kTermThreads, 0, s>>>(partial + (size_t)i * grid, grid, flags,
+                                                           gsum + op.rank);
+        }
+        if (sh.nccl) {
+          st = qwb::nccl_allgather_f64(ctx, gsum + sh.first_rank, gsum, 1, s);
+          if (st) return st;
+        }
+        term_global_finalize_kernel<<<1, 32, 0, s>>>(gsum, P, floor_, k, flags, flags + 1);
+      }
+      QWB_LAUNCH_CHECK(ctx, "sharded term kernels");
+      launched = upto;
+      QWB_CUDA(ctx, cudaMemcpyAsync(pin, flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+      QWB_CUDA(ctx, cudaStreamSynchronize(s));
+      done = pin[0] != 0;
+      chunk = 4;
+    }
+    prev_terms = pin[1];
+    if (terms_host) terms_host[sub] = pin[1];
+    cur = others[0];
+  }
+  if (cur != 0)
+    for (int i = 0; i < sh.nlocal; ++i)
+      QWB_CUDA(ctx, cudaMemcpyAsync(sh.bufs[i][0], sh.bufs[i][cur], nloc * sizeof(double2),
+                                    cudaMemcpyDeviceToDevice, s));
+  return QWB_OK;
+}
+
+int hc_stream_base(qwb_ctx* ctx, int dim, int S, double gamma, const uint32_t* bits, HcStream* op) {
+  if (dim < 1 || dim > 32) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "hypercube dim must be in 1..32");
+  if (S < 0 || S > kMaxShardBits) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "log2_shards must be in 0..%d", kMaxShardBits);
+  if (dim - S < hcs::LB)
+    QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "shards of hypercube(%d) over 2^%d ranks hold < 2^%d vertices", dim, S,
+             hcs::LB);
+  static int variant = -1;
+  if (variant < 0) {
+    const char* e = getenv("QWB_HC_STREAM");
+    variant = (e && *e) ? atoi(e) : 20801;
+  }
+  const int64_t ntiles = 1LL << (dim - S - hcs::LB);
+  *op = HcStream{};
+  op->dim = dim;
+  op->dim_loc = dim - S;
+  op->gamma = gamma;
+  op->bits = bits;
+  op->grid = (int)(ntiles < ctx->num_sms ? ntiles : ctx->num_sms);
+  op->device = ctx->device;
+  op->variant = variant;
+  return QWB_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+int qwb_taylor_evolve_hypercube_sharded(qwb_ctx* ctx, int dim, int log2_shards, double gamma,
+                                        const uint32_t* marked_bits, qwb_z* psi, qwb_z* work, int64_t substeps,
+                                        double tau, double floor, int max_terms, int* terms_host, void* stream) {
+  QWB_BEGIN(ctx);
+  HcStream base;
+  int st = hc_stream_base(ctx, dim, log2_shards, gamma, marked_bits, &base);
+  if (st) return st;
+  if (!ctx->comm) QWB_FAIL(ctx, QWB_E_NCCL, "qwb_comm_init has not been called");
+  if (ctx->nranks != (1 << log2_shards))
+    QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "communicator has %d ranks, expected 2^%d", ctx->nranks, log2_shards);
+  const int64_t nloc = 1LL << base.dim_loc;
+  ShardSet sh{};
+  sh.nlocal = 1;
+  sh.first_rank = ctx->rank;
+  sh.nccl = true;
+  double2* w = reinterpret_cast<double2*>(work);
+  sh.bufs[0][0] = reinterpret_cast<double2*>(psi);
+  for (int b = 1; b < 4; ++b) sh.bufs[0][b] = w + (b - 1) * nloc;
+  for (int j = 0; j < log2_shards; ++j) sh.recv[j] = w + (3 + j) * nloc;
+  return evolve_hc_sharded(ctx, base, log2_shards, sh, substeps, tau, floor, max_terms, terms_host,
+                           qwb::as_stream(stream));
+}
+
+int qwb_taylor_evolve_hypercube_shards_local(qwb_ctx* ctx, int dim, int log2_shards, double gamma,
+                                             const uint32_t* marked_bits, qwb_z* const* psi_host,
+                                             qwb_z* const* work_host, int64_t substeps, double tau, double floor,
+                                             int max_terms, int* terms_host, void* stream) {
+  QWB_BEGIN(ctx);
+  HcStream base;
+  int st = hc_stream_base(ctx, dim, log2_shards, gamma, marked_bits, &base);
+  if (st) return st;
+  const int64_t nloc = 1LL << base.dim_loc;
+  ShardSet sh{};
+  sh.nlocal = 1 << log2_shards;
+  sh.first_rank = 0;
+  sh.nccl = false;
+  for (int i = 0; i < sh.nlocal; ++i) {
+    double2* w = reinterpret_cast<double2*>(work_host[i]);
+    sh.bufs[i][0] = reinterpret_cast<double2*>(psi_host[i]);
+    for (int b = 1; b < 4; ++b) sh.bufs[i][b] = w + (b - 1) * nloc;
+  }
+  return evolve_hc_sharded(ctx, base, log2_shards, sh, substeps, tau, floor, max_terms, terms_host,
+                           qwb::as_stream(stream));
+}
 
 int qwb_taylor_evolve_csr(qwb_ctx* ctx, int64_t n, const int64_t* row_offsets, const int32_t* col,
                           const qwb_z* val, qwb_z* psi, qwb_z* work, int64_t substeps, double tau,
@@ -882,14 +1102,9 @@ int qwb_taylor_evolve_hypercube(qwb_ctx* ctx, int dim, double gamma, const uint3
     return evolve(ctx, op, n, p, w, substeps, tau, floor, max_terms, terms_host, s);
   }
   if (tiled == 3 && dim >= hcs::LB) {
-    static int variant = -1;
-    if (variant < 0) {
-      const char* e = getenv("QWB_HC_STREAM");
-      variant = (e && *e) ? atoi(e) : 20801;
-    }
-    const int64_t ntiles = n >> hcs::LB;
-    HcStream op{dim, gamma, marked_bits, (int)(ntiles < ctx->num_sms ? ntiles : ctx->num_sms), ctx->device,
-                variant};
+    HcStream op;
+    int st = hc_stream_base(ctx, dim, 0, gamma, marked_bits, &op);
+    if (st) return st;
     return evolve(ctx, op, n, p, w, substeps, tau, floor, max_terms, terms_host, s);
   }
   if (tiled == 2 && dim >= 10) {

@@ -1,4 +1,5 @@
-"""Multi-GPU coined walk: one periodic lattice split into y-slabs, one per rank.
+"""Multi-GPU walks: a periodic lattice split into y-slabs (coined walk), and a
+hypercube split into 2^S vertex shards (continuous-time walk).
 
 No reference counterpart (the reference's only parallelism is the in-process
 row-block pool, backend.py:426-430; multi-GPU is future work).
@@ -10,13 +11,21 @@ overlapped with the interior rows).  Results are bitwise equal to the
 single-GPU run because every arc is computed with the same formula and the
 position classes use global coordinates.
 
-The plan (`slab_partition`, `neighbours`) is plain Python so it is tested on
-CPU with the gloo backend (tests/test_distributed_cpu.py).
+The hypercube CTQW shards vertex v to rank v >> (dim - S):
+every Taylor term exchanges the local term slice with the S partner ranks
+r ^ 2^j (NCCL grouped send/recv inside `qwb_taylor_evolve_hypercube_sharded`)
+and all-gathers one float64 for the stop test; NVLink-bound by construction
+(S x 16 B x 2^(dim-S) per rank per term against ~64 B x 2^(dim-S) of HBM).
+
+The plans (`slab_partition`, `neighbours`, `hypercube_shard`,
+`hypercube_partners`) are plain Python so they are tested on CPU with the gloo
+backend (tests/test_distributed_cpu.py).
 """
 
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 
 import numpy as np
@@ -63,6 +72,140 @@ def _nccl_path() -> str | None:
     return None
 
 
+def hypercube_shard(dim: int, world: int, rank: int) -> tuple[int, int]:
+    """Vertex range [lo, hi) of `rank` when hypercube(dim) is split over
+    `world` = 2^S ranks: the vertices whose top S bits equal rank."""
+    S = _log2_world(world)
+    if dim - S < 10:
+        raise DimensionMismatch(f"hypercube({dim}) over {world} ranks leaves shards < 2^10 vertices")
+    if not (0 <= rank < world):
+        raise ValueError(f"rank {rank} not in 0..{world - 1}")
+    n = 1 << (dim - S)
+    return rank * n, (rank + 1) * n
+
+
+def hypercube_partners(rank: int, world: int) -> list[int]:
+    """Ranks holding the neighbours across each rank bit j: rank ^ 2^j."""
+    return [rank ^ (1 << j) for j in range(_log2_world(world))]
+
+
+def _log2_world(world: int) -> int:
+    if world < 1 or world & (world - 1):
+        raise ValueError(f"world size {world} is not a power of two")
+    return world.bit_length() - 1
+
+
+def _init_comm(engine: Engine, rank: int, world: int, group=None) -> None:
+    """NCCL communicator inside libqwb200 (torch.distributed only carries the id)."""
+    import torch.distributed as dist
+    lib = N.load()
+    path = _nccl_path()
+    if path and not os.environ.get("QWB_NCCL_LIB"):
+        os.environ["QWB_NCCL_LIB"] = path
+    uid = C.create_string_buffer(128)
+    if rank == 0:
+        N.check(lib.qwb_comm_unique_id(uid))
+    obj = [uid.raw if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    uid = C.create_string_buffer(obj[0], 128)
+    engine.call("qwb_comm_init", uid, world, rank)
+
+
+def _hypercube_setup(engine: Engine, dim: int, gamma: float, marked):
+    import torch
+    from . import ctqw as CT
+    marked = sorted(int(v) for v in marked)
+    n = 1 << dim
+    for v in marked:
+        if not (0 <= v < n):
+            from .errors import MarkedVertexOutOfRange
+            raise MarkedVertexOutOfRange(f"marked vertex {v} not in 0..{n - 1}")
+    bits = None
+    if marked:
+        bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=engine.torch_device)
+        mk = torch.tensor(marked, dtype=torch.int64, device=engine.torch_device)
+        engine.call("qwb_marked_bitmap", n, N.ptr(mk), len(marked), N.ptr(bits), engine.stream())
+    inf_norm = CT._inf_norm_hypercube(engine, dim, float(gamma), marked)
+    return bits, inf_norm
+
+
+class ShardedHypercubeWalk:
+    """This rank's shard of a continuous-time walk on hypercube(dim),
+    H = -gamma A - sum_M |v><v| (ctqw.py:84-98).  Call collectively."""
+
+    def __init__(self, engine: Engine, dim: int, gamma: float, marked=(), rank: int = 0, world: int = 1,
+                 group=None):
+        self.engine = engine
+        self.dim, self.gamma = int(dim), float(gamma)
+        self.rank, self.world = int(rank), int(world)
+        self.S = _log2_world(self.world)
+        self.lo, self.hi = hypercube_shard(self.dim, self.world, self.rank)
+        self.n_local = self.hi - self.lo
+        self.group = group
+        self.bits, self.inf_norm = _hypercube_setup(engine, self.dim, self.gamma, marked)
+        self.work = empty_z(engine, (3 + self.S) * self.n_local)
+        if self.world > 1:
+            _init_comm(engine, self.rank, self.world, group)
+
+    def global_norm(self, psi_local) -> float:
+        from .backend import device_norm
+        local = device_norm(self.engine, psi_local) ** 2
+        if self.world == 1:
+            return math.sqrt(local)
+        import torch.distributed as dist
+        parts = [None] * self.world
+        dist.all_gather_object(parts, local, group=self.group)
+        return math.sqrt(sum(parts))
+
+    def evolve(self, psi_local, t: float, tol: float = 1e-12) -> list[int]:
+        """psi_local (device, in place) <- this rank's slice of exp(-iHt) psi;
+        returns the term count of each sub-step (the same on every rank)."""
+        from . import ctqw as CT
+        if t == 0:
+            return []
+        substeps = max(1, math.ceil(self.inf_norm * abs(t)))
+        tau = t / substeps
+        floor = tol * self.global_norm(psi_local)
+        terms = (C.c_int * substeps)()
+        eng = self.engine
+        if self.world == 1:
+            eng.call("qwb_taylor_evolve_hypercube", self.dim, self.gamma, N.ptr(self.bits), N.ptr(psi_local),
+                     N.ptr(self.work), substeps, tau, floor, int(CT._MAX_SERIES_TERMS), terms, eng.stream())
+        else:
+            eng.call("qwb_taylor_evolve_hypercube_sharded", self.dim, self.S, self.gamma, N.ptr(self.bits),
+                     N.ptr(psi_local), N.ptr(self.work), substeps, tau, floor, int(CT._MAX_SERIES_TERMS),
+                     terms, eng.stream())
+        return list(terms)
+
+    def close(self) -> None:
+        if self.world > 1:
+            self.engine.call("qwb_comm_destroy")
+
+
+def emulate_hypercube_shards(engine: Engine, dim: int, gamma: float, marked, world: int, psi: np.ndarray,
+                             t: float, tol: float = 1e-12):
+    """Run the hypercube shard decomposition for `world` shards on ONE device
+    (partner slices read in place of the NCCL exchange); returns (full state,
+    terms per sub-step).  Test hook for the multi-GPU CTQW path."""
+    import torch
+    from . import ctqw as CT
+    S = _log2_world(world)
+    bits, inf_norm = _hypercube_setup(engine, dim, gamma, marked)
+    full = torch.from_numpy(np.ascontiguousarray(psi, dtype=np.complex128)).to(engine.torch_device)
+    nl = (1 << dim) >> S
+    shards = [full[r * nl:(r + 1) * nl].clone() for r in range(world)]
+    works = [empty_z(engine, 3 * nl) for _ in range(world)]
+    substeps = max(1, math.ceil(inf_norm * abs(t)))
+    tau = t / substeps
+    floor = tol * float(np.linalg.norm(psi))
+    terms = (C.c_int * substeps)()
+    ps = (C.c_void_p * world)(*[N.ptr(x) for x in shards])
+    ws = (C.c_void_p * world)(*[N.ptr(x) for x in works])
+    engine.call("qwb_taylor_evolve_hypercube_shards_local", dim, S, float(gamma), N.ptr(bits), ps, ws, substeps,
+                tau, floor, int(CT._MAX_SERIES_TERMS), terms, engine.stream())
+    return torch.cat(shards).cpu().numpy(), list(terms)
+
+
 class SlabLattice:
     """This rank's slab of a periodic nx x ny lattice walk (flip-flop or
     persistent shift, optional marked vertices).  Call collectively."""
@@ -70,7 +213,6 @@ class SlabLattice:
     def __init__(self, engine: Engine, nx: int, ny: int, shift: str = "flipflop", marked=(),
                  rank: int = 0, world: int = 1, group=None):
         import torch
-        import torch.distributed as dist
         self.engine = engine
         self.nx, self.ny = int(nx), int(ny)
         self.rank, self.world = int(rank), int(world)
@@ -89,17 +231,7 @@ class SlabLattice:
         self.a.zero_()
         self.b.zero_()
         if self.world > 1:
-            lib = N.load()
-            path = _nccl_path()
-            if path and not os.environ.get("QWB_NCCL_LIB"):
-                os.environ["QWB_NCCL_LIB"] = path
-            uid = C.create_string_buffer(128)
-            if self.rank == 0:
-                N.check(lib.qwb_comm_unique_id(uid))
-            obj = [uid.raw if self.rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0, group=group)
-            uid = C.create_string_buffer(obj[0], 128)
-            engine.call("qwb_comm_init", uid, self.world, self.rank)
+            _init_comm(engine, self.rank, self.world, group)
 
     def load(self, owned_arcs) -> None:
         """owned_arcs: device tensor of this slab's arcs (reference order)."""

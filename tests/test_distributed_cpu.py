@@ -122,3 +122,95 @@ def test_gloo_multiprocess_halo_exchange(tmp_path, world, shift):
     u = O.evolution_operator(offs, cols, shift, marked, "grid", (nx, ny, True))
     ref = O.coined_simulate(u, _psi(4 * nx * ny, 3), [steps])[0]
     assert np.array_equal(got, ref)
+
+
+# ---------------------------------------------------------------------------
+# hypercube CTQW shards: vertex v -> rank v >> (dim - S);
+# per Taylor term each rank exchanges its term slice with partners r ^ 2^j
+# and the stop test uses the all-gathered norm.  The model below runs that
+# plan in real processes over gloo with the oracle's row arithmetic
+# (oracle.csr_rows restates numpy's gather-multiply-reduceat), and must equal
+# the oracle's single-process evolve bitwise.
+# ---------------------------------------------------------------------------
+
+def test_hypercube_plan():
+    assert DI.hypercube_shard(12, 4, 2) == (2048, 3072)
+    assert DI.hypercube_partners(5, 8) == [4, 7, 1]
+    assert DI.hypercube_partners(0, 1) == []
+    with pytest.raises(Exception):
+        DI.hypercube_shard(12, 3, 0)          # not a power of two
+    with pytest.raises(Exception):
+        DI.hypercube_shard(11, 4, 0)          # shards < 2^10 vertices
+    # every neighbour of a shard's vertex is local or in exactly one partner shard
+    dim, world = 12, 4
+    for r in range(world):
+        lo, hi = DI.hypercube_shard(dim, world, r)
+        owners = {((v ^ (1 << b)) >> (dim - 2)) for v in range(lo, hi, 97) for b in range(dim)}
+        assert owners == {r, *DI.hypercube_partners(r, world)}
+
+
+def _hc_worker(rank, world, port, dim, gamma, marked, t, out_dir):
+    import math
+
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    offs, cols = O.hypercube_adjacency(dim)
+    h = O.hamiltonian(offs, cols, gamma, marked)
+    n = 1 << dim
+    psi = _psi(n, dim)
+    lo, hi = DI.hypercube_shard(dim, world, rank)
+    partners = DI.hypercube_partners(rank, world)
+    cur = psi[lo:hi].copy()
+    substeps = max(1, math.ceil(O.inf_norm(h) * abs(t)))
+    tau = t / substeps
+    floor = 1e-12 * float(np.linalg.norm(psi))
+    view = np.zeros(n, dtype=np.complex128)
+    terms = []
+    for _ in range(substeps):
+        acc, term = cur.copy(), cur.copy()
+        for k in range(1, 1000):
+            # exchange the term slice with every partner (one grouped round)
+            send = torch.from_numpy(term.view(np.float64).copy())
+            recvs = [torch.empty_like(send) for _ in partners]
+            ops = []
+            for p, rv in zip(partners, recvs):
+                ops += [dist.P2POp(dist.isend, send, p), dist.P2POp(dist.irecv, rv, p)]
+            for r in (dist.batch_isend_irecv(ops) if ops else []):
+                r.wait()
+            view[lo:hi] = term
+            for p, rv in zip(partners, recvs):
+                plo, phi = DI.hypercube_shard(dim, world, p)
+                view[plo:phi] = rv.numpy().view(np.complex128)
+            hterm = O.csr_rows(h, view, lo, hi)
+            term = complex(-1j * tau / k) * hterm
+            acc = acc + complex(1.0) * term
+            parts = [None] * world
+            dist.all_gather_object(parts, float(np.vdot(term, term).real))
+            if math.sqrt(sum(parts)) <= floor:
+                terms.append(k)
+                break
+        cur = acc
+    np.save(os.path.join(out_dir, f"shard{rank}.npy"), cur)
+    np.save(os.path.join(out_dir, f"terms{rank}.npy"), np.array(terms))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,marked", [(2, (3, 1500)), (4, (0,))])
+def test_gloo_multiprocess_hypercube_shards(tmp_path, world, marked):
+    import torch.multiprocessing as mp
+    dim, gamma, t = 12, 1.0 / 12, 0.8
+    port = _free_port()
+    mp.start_processes(_hc_worker, args=(world, port, dim, gamma, marked, t, str(tmp_path)),
+                       nprocs=world, join=True, start_method="spawn")
+    got = np.concatenate([np.load(tmp_path / f"shard{r}.npy") for r in range(world)])
+    terms = [list(np.load(tmp_path / f"terms{r}.npy")) for r in range(world)]
+    assert all(tr == terms[0] for tr in terms)
+    offs, cols = O.hypercube_adjacency(dim)
+    stats = []
+    ref = O.evolve_state(O.hamiltonian(offs, cols, gamma, marked), _psi(1 << dim, dim), t, stats=stats)
+    assert terms[0] == stats
+    assert np.array_equal(got, ref)
