@@ -487,6 +487,27 @@ def measure_extras(q, CO, eng, dev, peak):
                               "us_per_step": per * 1e6}
     del r
     torch.cuda.empty_cache()
+    # C3 in full: 4096^2, centre marked, uniform psi0 (= 2^-13 exactly),
+    # T = ceil(sqrt(N ln N)) = 16707 steps, p(marked) after every step fused
+    # into the step kernels, full distributions every 4096 steps
+    import math
+    N = nx * nx
+    T = math.ceil(math.sqrt(N * math.log(N)))
+    psi_u = q.WalkState(q.graphs.arc_basis(g), np.full(arcs, 2.0 ** -13, dtype=np.complex128))
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    trace, dists = CO.search_trace(eng, spec, T, psi_u, 4096)
+    torch.cuda.synchronize(dev)
+    dt = time.perf_counter() - t0
+    pk = int(np.argmax(trace[:, 0]))
+    out["c3_search_grid4096"] = {"steps": T, "seconds": dt, "arc_updates_per_s": arcs * T / dt,
+                                 "p_marked_peak": float(trace[pk, 0]), "peak_step": pk,
+                                 "p_marked_final": float(trace[-1, 0]), "uniform_p": 1.0 / N,
+                                 "distributions_saved": sorted(dists),
+                                 "call": "coined.search_trace(engine, spec, 16707, uniform psi0, 4096) "
+                                         "incl. H2D, layout conversion, trace D2H"}
+    del trace, dists, psi_u
+    torch.cuda.empty_cache()
     # K1: device-built CSR U at 2048^2, SpMV per step (120 B/arc algorithmic)
     nx = 2048
     g = q.graphs.grid(nx, nx)

@@ -55,12 +55,25 @@ struct TbShape {
   static constexpr size_t smem_bytes() { return (4 * (size_t)REG + 4 * (size_t)NT) * sizeof(double2); }
 };
 
-// p(v) per step for up to 8 traced vertices (search runs): out[t * n + k]
+// p(v) per step for up to 8 traced vertices (search runs): out[t * n + k];
+// x, y: the vertices' coordinates (host-computed, no division on the device)
 struct TraceList {
   int n;
   int64_t v[8];
+  int x[8], y[8];
   double* out;
 };
+
+// p of a traced vertex from its level-t (doubled-space) amplitudes: unscale,
+// reference slot order, numpy |z|^2 and row sum.  Out of line: only the
+// thread owning a traced vertex calls it, the hot loops keep their code size.
+__device__ __noinline__ void trace_emit(int gx, int gy, int nx, int ny, double sc, double2 vD, double2 vL,
+                                        double2 vR, double2 vU, double* out) {
+  const auto un = [&](double2 a) { return make_double2(__dmul_rn(a.x, sc), __dmul_rn(a.y, sc)); };
+  const qwb::Slots o = qwb::order_slots(gx, gy, nx, ny, un(vD), un(vL), un(vR), un(vU));
+  const double m0 = qwb::abs2_np(o.s0), m1 = qwb::abs2_np(o.s1), m2 = qwb::abs2_np(o.s2), m3 = qwb::abs2_np(o.s3);
+  *out = __dadd_rn(m0, __dadd_rn(__dadd_rn(m1, m2), m3));
+}
 
 // T steps of a tile on chip (see the file comment).  INTERIOR: every vertex of
 // the region is an unmarked, untraced interior vertex (no slot permutation, no
@@ -88,14 +101,12 @@ __device__ __forceinline__ void tile_steps(int nx, int ny, int gx, const int (&g
       for (int j = 0; j < V; ++j) {
         if (!own[j]) continue;
         const int64_t wg = (int64_t)gy[j] * nx + gx;
-        for (int k = 0; k < tr.n; ++k) {
-          if (tr.v[k] != wg) continue;
-          const double sc = 1.0 / (double)(1 << t);   // level t holds 2^t psi_t
-          const auto un = [&](double2 a) { return make_double2(__dmul_rn(a.x, sc), __dmul_rn(a.y, sc)); };
-          const qwb::Slots o = qwb::order_slots(gx, gy[j], nx, ny, un(vD[j]), un(vL[j]), un(vR[j]), un(vU[j]));
-          const double m0 = qwb::abs2_np(o.s0), m1 = qwb::abs2_np(o.s1), m2 = qwb::abs2_np(o.s2),
-                       m3 = qwb::abs2_np(o.s3);
-          tr.out[t * tr.n + k] = __dadd_rn(m0, __dadd_rn(__dadd_rn(m1, m2), m3));
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {   // static indices: tr stays in the param space
+          if (k >= tr.n || tr.v[k] != wg) continue;
+          // level t holds 2^t psi_t
+          trace_emit(gx, gy[j], nx, ny, 1.0 / (double)(1 << t), vD[j], vL[j], vR[j], vU[j],
+                     tr.out + t * tr.n + k);
         }
       }
     }
@@ -139,6 +150,7 @@ __device__ __forceinline__ void tile_steps(int nx, int ny, int gx, const int (&g
 struct MarkedList {   // up to 8 marked vertex ids; n < 0: more than 8 (use the bitmap)
   int n;
   int64_t v[8];
+  int x[8], y[8];     // their coordinates (host-computed)
 };
 
 template <int SHIFT, bool MARKED, int T, int BY, int V, bool TRACE>
@@ -195,8 +207,7 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
     cp_commit();
     // regions that touch no torus edge and hold no marked or traced vertex run
     // a branch-free specialisation: every vertex is interior (slot order D L R U)
-    auto in_region = [&](int64_t w) {
-      const int mx = (int)(w % nx), my = (int)(w / nx);
+    auto in_region = [&](int mx, int my) {
       return mx >= x0 - T && mx < x0 - T + 32 && my >= y0 - T && my < y0 - T + S::RY;
     };
     bool interior = x0 - T >= 1 && x0 - T + 31 <= nx - 2 && y0 - T >= 1 &&
@@ -205,11 +216,13 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
       if (mk.n < 0) {
         interior = false;   // too many marked vertices for the list: general path
       } else {
-        for (int k = 0; k < mk.n; ++k) interior &= !in_region(mk.v[k]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) interior &= (k >= mk.n) || !in_region(mk.x[k], mk.y[k]);
       }
     }
     if (TRACE)
-      for (int k = 0; k < tr.n; ++k) interior &= !in_region(tr.v[k]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) interior &= (k >= tr.n) || !in_region(tr.x[k], tr.y[k]);
     const bool col_ok = tx >= T && tx < T + OX && x0 + tx - T < nx;
     bool own[V];
 #pragma unroll
@@ -457,11 +470,19 @@ int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx
   if (depth > 6) depth = 6;
   MarkedList mk{};
   mk.n = n_marked <= 8 ? (int)n_marked : -1;
-  for (int k = 0; k < mk.n; ++k) mk.v[k] = marked_host[k];
+  for (int k = 0; k < mk.n; ++k) {
+    mk.v[k] = marked_host[k];
+    mk.x[k] = (int)(marked_host[k] % nx);
+    mk.y[k] = (int)(marked_host[k] / nx);
+  }
   TraceList tl{};
   tl.n = trace ? n_trace : 0;
   tl.out = trace;
-  for (int k = 0; k < tl.n; ++k) tl.v[k] = trace_vertices_host[k];
+  for (int k = 0; k < tl.n; ++k) {
+    tl.v[k] = trace_vertices_host[k];
+    tl.x[k] = (int)(trace_vertices_host[k] % nx);
+    tl.y[k] = (int)(trace_vertices_host[k] / nx);
+  }
   // shape 1: 32x16 threads, 2 rows each (32x32 region); 2: 32x24 threads, 2 rows
   // each (32x48 region); 3: 32x16 threads, 3 rows each (32x48 region)
 #define QWB_TB_CASE(T_)                                                                        \
