@@ -168,9 +168,20 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
   const int tid = ty * 32 + tx;
   const int64_t n = (int64_t)nx * ny;
 
-  auto prefetch = [&](int tile) {
-    const int bx = (tile % tiles_x) * OX - T + tx;
-    const int by = (tile / tiles_x) * OY - T + ty * V;
+  // tile coordinates advance by gridDim.x tiles per iteration: (gdiv, gmod)
+  // rows / columns, carried without a division per tile
+  const int gdiv = (int)gridDim.x / tiles_x, gmod = (int)gridDim.x % tiles_x;
+  auto advance = [&](int& c, int& r) {
+    c += gmod;
+    r += gdiv;
+    if (c >= tiles_x) {
+      c -= tiles_x;
+      ++r;
+    }
+  };
+  auto prefetch = [&](int tcol, int trow) {
+    const int bx = tcol * OX - T + tx;
+    const int by = trow * OY - T + ty * V;
     const int gx = wrapc(bx, nx);
 #pragma unroll
     for (int j = 0; j < V; ++j) {
@@ -184,10 +195,12 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
 
   int tile = blockIdx.x;
   if (tile >= ntiles) return;
-  prefetch(tile);
+  int tcol = tile % tiles_x, trow = tile / tiles_x;
+  prefetch(tcol, trow);
   cp_commit();
   for (; tile < ntiles; tile += gridDim.x) {
-    const int x0 = (tile % tiles_x) * OX, y0 = (tile / tiles_x) * OY;
+    const int x0 = tcol * OX, y0 = trow * OY;
+    advance(tcol, trow);   // (tcol, trow) now hold the next tile's coordinates
     const int gx = wrapc(x0 - T + tx, nx);
     int gy[V];
     double2 vD[V], vL[V], vR[V], vU[V];
@@ -203,7 +216,7 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
       vU[j] = stage[3 * S::REG + li];
     }
     __syncthreads();
-    if (tile + (int)gridDim.x < ntiles) prefetch(tile + gridDim.x);
+    if (tile + (int)gridDim.x < ntiles) prefetch(tcol, trow);
     cp_commit();
     // regions that touch no torus edge and hold no marked or traced vertex run
     // a branch-free specialisation: every vertex is interior (slot order D L R U)
