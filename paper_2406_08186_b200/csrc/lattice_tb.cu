@@ -52,7 +52,12 @@ struct TbShape {
   static constexpr int RY = BY * V;        // region rows
   static constexpr int NT = 32 * BY;       // threads
   static constexpr int REG = RX * RY;      // region vertices
-  static constexpr size_t smem_bytes() { return (4 * (size_t)REG + 4 * (size_t)NT) * sizeof(double2); }
+  // stages of the next tiles' amplitudes: two (loads of two tiles in flight)
+  // when they fit next to the exchange buffers, else one
+  static constexpr int NSTAGE = ((8 * (size_t)REG + 4 * (size_t)NT) * sizeof(double2) <= 232448) ? 2 : 1;
+  static constexpr size_t smem_bytes() {
+    return (4 * (size_t)REG * NSTAGE + 4 * (size_t)NT) * sizeof(double2);
+  }
 };
 
 // p(v) per step for up to 8 traced vertices (search runs): out[t * n + k];
@@ -161,8 +166,8 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
   using S = TbShape<BY, V>;
   constexpr int OX = S::RX - 2 * T, OY = S::RY - 2 * T;   // exact (owned) block
   extern __shared__ double2 sm[];
-  double2* stage = sm;                 // [4][RY][RX] next tile's amplitudes
-  double2* xD = sm + 4 * S::REG;       // [2][BY][32] O_D of each thread's lowest row
+  double2* stage0 = sm;                // [NSTAGE][4][RY][RX] next tiles' amplitudes
+  double2* xD = sm + 4 * S::REG * S::NSTAGE;   // [2][BY][32] O_D of each thread's lowest row
   double2* xU = xD + 2 * S::NT;        // [2][BY][32] O_U of each thread's highest row
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * 32 + tx;
@@ -179,7 +184,7 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
       ++r;
     }
   };
-  auto prefetch = [&](int tcol, int trow) {
+  auto prefetch = [&](double2* stage, int tcol, int trow) {
     const int bx = tcol * OX - T + tx;
     const int by = trow * OY - T + ty * V;
     const int gx = wrapc(bx, nx);
@@ -196,15 +201,25 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
   int tile = blockIdx.x;
   if (tile >= ntiles) return;
   int tcol = tile % tiles_x, trow = tile / tiles_x;
-  prefetch(tcol, trow);
-  cp_commit();
-  for (; tile < ntiles; tile += gridDim.x) {
+  // (pcol, prow): the tile the next prefetch loads, NSTAGE - 1 tiles ahead of (tcol, trow)
+  int pcol = tcol, prow = trow, ptile = tile;
+  for (int k = 0; k < S::NSTAGE; ++k) {
+    if (ptile < ntiles) prefetch(stage0 + (size_t)k * 4 * S::REG, pcol, prow);
+    cp_commit();
+    advance(pcol, prow);
+    ptile += gridDim.x;
+  }
+  for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
+    double2* stage = stage0 + (size_t)(S::NSTAGE == 2 ? (it & 1) : 0) * 4 * S::REG;
     const int x0 = tcol * OX, y0 = trow * OY;
-    advance(tcol, trow);   // (tcol, trow) now hold the next tile's coordinates
+    advance(tcol, trow);
     const int gx = wrapc(x0 - T + tx, nx);
     int gy[V];
     double2 vD[V], vL[V], vR[V], vU[V];
-    cp_wait_all();
+    if (S::NSTAGE == 2)
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");   // this tile's group; the next may fly
+    else
+      cp_wait_all();
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < V; ++j) {
@@ -216,8 +231,10 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
       vU[j] = stage[3 * S::REG + li];
     }
     __syncthreads();
-    if (tile + (int)gridDim.x < ntiles) prefetch(tcol, trow);
+    if (ptile < ntiles) prefetch(stage, pcol, prow);   // into the stage just consumed
     cp_commit();
+    advance(pcol, prow);
+    ptile += gridDim.x;
     // regions that touch no torus edge and hold no marked or traced vertex run
     // a branch-free specialisation: every vertex is interior (slot order D L R U)
     auto in_region = [&](int mx, int my) {
