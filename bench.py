@@ -368,7 +368,7 @@ def run_b200(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cpu = cpu_reference(nx, 8, os.cpu_count() or 1)
+            cpu = cpu_reference(nx, 64, os.cpu_count() or 1)   # ~10 s of host work
         except Exception as e:  # pragma: no cover - reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                    "sample": f"failed: {e!r}"}
