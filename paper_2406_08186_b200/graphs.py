@@ -223,9 +223,50 @@ def hypercube(dim: int) -> Graph:
     return Graph(1 << dim, None, "hypercube", (int(dim),))
 
 
+# ---------------------------------------------------------------------------
+# closed forms for the regular families (graphs.py:115-159): a vertex's sorted
+# neighbours and its arc-span start without materialising the adjacency (a
+# host copy of the 8192^2 torus adjacency is 2 GB; ket() needs one index)
+# ---------------------------------------------------------------------------
+
+def _closed_form(g: Graph) -> bool:
+    if not g._generated or g._adjacency is not None:
+        return False
+    if g.kind == "grid":
+        return g.is_torus
+    return g.kind in ("cycle", "line", "hypercube")
+
+
+def _family_neighbors(g: Graph, v: int) -> list[int]:
+    if g.kind == "grid":
+        nx, ny, _ = g.params
+        x, y = v % nx, v // nx
+        cand = {((x + 1) % nx) + nx * y, ((x - 1) % nx) + nx * y, x + nx * ((y + 1) % ny), x + nx * ((y - 1) % ny)}
+        return sorted(cand)
+    if g.kind == "cycle":
+        n = g.n
+        return sorted({(v - 1) % n, (v + 1) % n})
+    if g.kind == "line":
+        return [u for u in (v - 1, v + 1) if 0 <= u < g.n]
+    dim = g.params[0]   # hypercube: v xor 2^b, ascending
+    return sorted(v ^ (1 << b) for b in range(dim))
+
+
+def _family_row_offset(g: Graph, v: int) -> int:
+    if g.kind == "grid":
+        return 4 * v
+    if g.kind == "cycle":
+        return 2 * v
+    if g.kind == "line":
+        return 0 if v == 0 else 2 * v - 1
+    return g.params[0] * v
+
+
 def neighbors(g: Graph, v: int) -> np.ndarray:
     if not (0 <= v < g.n):
         raise VertexOutOfRange(f"vertex {v} not in 0..{g.n - 1}")
+    if _closed_form(g):
+        return np.asarray(_family_neighbors(g, int(v)), dtype=np.int64)
     a = g.adjacency
     return a.col_indices[a.row_offsets[v]: a.row_offsets[v + 1]].copy()
 
@@ -233,6 +274,8 @@ def neighbors(g: Graph, v: int) -> np.ndarray:
 def degree(g: Graph, v: int) -> int:
     if not (0 <= v < g.n):
         raise VertexOutOfRange(f"vertex {v} not in 0..{g.n - 1}")
+    if _closed_form(g):
+        return len(_family_neighbors(g, int(v)))
     a = g.adjacency
     return int(a.row_offsets[v + 1] - a.row_offsets[v])
 
@@ -286,6 +329,11 @@ def arc_index(b: ArcBasis, v: int, w: int) -> int:
     g = b.graph
     if not (0 <= v < g.n):
         raise NotAnArc(f"({v}, {w}) is not an arc of the graph")
+    if _closed_form(g):
+        nb = _family_neighbors(g, v)
+        if w not in nb:
+            raise NotAnArc(f"({v}, {w}) is not an arc of the graph")
+        return _family_row_offset(g, v) + nb.index(w)
     a = g.adjacency
     lo, hi = int(a.row_offsets[v]), int(a.row_offsets[v + 1])
     j = lo + int(np.searchsorted(a.col_indices[lo:hi], w))

@@ -129,3 +129,30 @@ def test_host_csr_from_triplets_matches_oracle(oracle):
         q.graphs.graph_from_adjacency([[1, 1], [1, 0]])
     with pytest.raises(q.errors.WeightedAdjacency):
         q.graphs.graph_from_adjacency([[0, 2], [2, 0]])
+
+
+def test_family_closed_forms_match_oracle():
+    """arc_index / neighbors / degree on the regular families without the
+    adjacency (closed forms, graphs.py:115-159 semantics) equal the oracle's
+    CSR for every vertex of small instances; no device is touched."""
+    from oracle import qwalk_oracle as O
+    import paper_2406_08186_b200 as q
+    cases = [(q.graphs.grid(5, 7), O.grid_adjacency(5, 7)), (q.graphs.grid(3, 3), O.grid_adjacency(3, 3)),
+             (q.graphs.cycle(9), O.cycle_adjacency(9)), (q.graphs.line(6), O.line_adjacency(6)),
+             (q.graphs.hypercube(5), O.hypercube_adjacency(5))]
+    for g, (offs, cols) in cases:
+        b = q.graphs.arc_basis(g)
+        for v in range(g.n):
+            nb = cols[offs[v]:offs[v + 1]]
+            assert np.array_equal(q.graphs.neighbors(g, v), nb), (g, v)
+            assert q.graphs.degree(g, v) == len(nb)
+            for j, w in enumerate(nb):
+                assert q.graphs.arc_index(b, v, int(w)) == offs[v] + j
+        with pytest.raises(q.errors.NotAnArc):
+            q.graphs.arc_index(b, 0, 0)
+        assert g._adjacency is None          # nothing was materialised
+    # a huge torus: an arc index is O(1) and needs no adjacency
+    big = q.graphs.grid(8192, 8192)
+    c = 4096 + 8192 * 4096
+    assert q.graphs.arc_index(q.graphs.arc_basis(big), c, c + 1) == 4 * c + 2
+    assert big._adjacency is None
