@@ -184,6 +184,16 @@ int qwb_slab_step(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_l
 /* single-device emulation of the per-step exchange between nslabs slabs (tests) */
 int qwb_slab_exchange_local(qwb_ctx* ctx, int64_t nx, int shift, const int64_t* ny_local_host,
                             qwb_z* const* planes_host, int nslabs, void* stream);
+/* Halo exchange of a row-partitioned CSR operator (generic graphs; the row
+ * ranges and index lists come from distributed.csr_partition).  x_ext =
+ * [own entries (n_local) | halo]; for peer i (peers_host[i], ascending): send
+ * x_ext[send_idx[send_off[i] .. send_off[i+1])] (device int64 indices) and
+ * receive recv_off[i+1] - recv_off[i] entries into x_ext[n_local + recv_off[i]
+ * ..], one NCCL group.  send_buf: send_off[npeers] qwb_z.  The step itself is
+ * qwb_spmv on the local rows (columns renumbered into x_ext).               */
+int qwb_csr_halo_exchange(qwb_ctx* ctx, int64_t n_local, qwb_z* x_ext, const int64_t* send_idx,
+                          const int64_t* send_off_host, const int64_t* recv_off_host, const int* peers_host,
+                          int npeers, qwb_z* send_buf, void* stream);
 /* NCCL communicator (one per rank; id: 128 bytes from rank 0, broadcast by the caller) */
 int qwb_comm_unique_id(void* id_out_host);
 int qwb_comm_init(qwb_ctx* ctx, const void* id_host, int nranks, int rank);

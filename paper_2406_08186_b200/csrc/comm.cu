@@ -104,6 +104,21 @@ int nccl_exchange(qwb_ctx* ctx, const void* send, void* const* recv, const int* 
   return QWB_OK;
 }
 
+// One grouped exchange with per-peer buffers and counts (float64s).
+int nccl_sendrecv_list(qwb_ctx* ctx, const void* const* send, const size_t* send_count, void* const* recv,
+                       const size_t* recv_count, const int* peers, int npeers, cudaStream_t s) {
+  if (!ctx->comm) QWB_FAIL(ctx, QWB_E_NCCL, "qwb_comm_init has not been called");
+  NcclComm comm = (NcclComm)ctx->comm;
+  QWB_NCCL(ctx, g_nccl.group_start());
+  for (int i = 0; i < npeers; ++i) {
+    if (send_count[i])
+      QWB_NCCL(ctx, g_nccl.send(const_cast<void*>(send[i]), send_count[i], kNcclFloat64, peers[i], comm, s));
+    if (recv_count[i]) QWB_NCCL(ctx, g_nccl.recv(recv[i], recv_count[i], kNcclFloat64, peers[i], comm, s));
+  }
+  QWB_NCCL(ctx, g_nccl.group_end());
+  return QWB_OK;
+}
+
 // recv[r * count ...] = rank r's send (count float64s), on stream s
 int nccl_allgather_f64(qwb_ctx* ctx, const double* send, double* recv, size_t count, cudaStream_t s) {
   if (!ctx->comm) QWB_FAIL(ctx, QWB_E_NCCL, "qwb_comm_init has not been called");
@@ -219,6 +234,43 @@ int qwb_slab_run(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_lo
   QWB_LAUNCH_CHECK(ctx, "lattice_step_kernel(slab run)");
   if (final_in_b_host) *final_in_b_host = (steps % 2) ? 1 : 0;
   return QWB_OK;
+}
+
+static __global__ void gather_z_kernel(int64_t n, const int64_t* __restrict__ idx, const double2* __restrict__ x,
+                                double2* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = x[idx[i]];
+}
+
+// Halo exchange of a row-partitioned CSR operator (distributed.csr_partition).
+// x_ext = [own entries (n_local) | halo]; for peer i: send x_ext[send_idx[
+// send_off[i] .. send_off[i+1])] and receive recv_off[i+1] - recv_off[i]
+// entries into x_ext[n_local + recv_off[i] ..].  send_buf: send_off[npeers]
+// qwb_z of scratch.
+int qwb_csr_halo_exchange(qwb_ctx* ctx, int64_t n_local, qwb_z* x_ext, const int64_t* send_idx,
+                          const int64_t* send_off_host, const int64_t* recv_off_host, const int* peers_host,
+                          int npeers, qwb_z* send_buf, void* stream) {
+  QWB_BEGIN(ctx);
+  if (npeers < 0 || npeers > 1024) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "bad peer count %d", npeers);
+  if (npeers == 0) return QWB_OK;
+  cudaStream_t s = qwb::as_stream(stream);
+  double2* xe = reinterpret_cast<double2*>(x_ext);
+  double2* sb = reinterpret_cast<double2*>(send_buf);
+  const int64_t nsend = send_off_host[npeers];
+  if (nsend > 0) {
+    gather_z_kernel<<<qwb::blocks_for(nsend, 256, (int64_t)ctx->num_sms * 8), 256, 0, s>>>(nsend, send_idx, xe, sb);
+    QWB_LAUNCH_CHECK(ctx, "gather_z_kernel");
+  }
+  const void* sp[1024];
+  void* rp[1024];
+  size_t sc[1024], rc[1024];
+  for (int i = 0; i < npeers; ++i) {
+    sp[i] = sb + send_off_host[i];
+    sc[i] = 2 * (size_t)(send_off_host[i + 1] - send_off_host[i]);
+    rp[i] = xe + n_local + recv_off_host[i];
+    rc[i] = 2 * (size_t)(recv_off_host[i + 1] - recv_off_host[i]);
+  }
+  return qwb::nccl_sendrecv_list(ctx, sp, sc, rp, rc, peers_host, npeers, s);
 }
 
 // Single-process emulation of the exchange for P slabs held on ONE device

@@ -37,6 +37,8 @@ int begin(qwb_ctx* ctx);   // checks ctx alive and sets the device
 int nccl_exchange(qwb_ctx* ctx, const void* send, void* const* recv, const int* peers, int npeers,
                   size_t count, cudaStream_t s);
 int nccl_allgather_f64(qwb_ctx* ctx, const double* send, double* recv, size_t count, cudaStream_t s);
+int nccl_sendrecv_list(qwb_ctx* ctx, const void* const* send, const size_t* send_count, void* const* recv,
+                       const size_t* recv_count, const int* peers, int npeers, cudaStream_t s);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

@@ -17,9 +17,16 @@ r ^ 2^j (NCCL grouped send/recv inside `qwb_taylor_evolve_hypercube_sharded`)
 and all-gathers one float64 for the stop test; NVLink-bound by construction
 (S x 16 B x 2^(dim-S) per rank per term against ~64 B x 2^(dim-S) of HBM).
 
+Any other graph (SURVEY §8(e) "generic-graph CSR"): the rows of U (= arcs,
+reference order) are split into contiguous, nnz-balanced ranges; each rank
+keeps its rows with columns renumbered into an extended vector [own entries |
+halo], and per step receives exactly the halo entries its rows read from each
+peer (precomputed send/recv index lists, one NCCL group), then runs the CSR
+SpMV kernel on its rows: the single-GPU arithmetic, so bitwise equal.
+
 The plans (`slab_partition`, `neighbours`, `hypercube_shard`,
-`hypercube_partners`) are plain Python so they are tested on CPU with the gloo
-backend (tests/test_distributed_cpu.py).
+`hypercube_partners`, `csr_partition`) are plain Python so they are tested on
+CPU with the gloo backend (tests/test_distributed_cpu.py).
 """
 
 from __future__ import annotations
@@ -93,6 +100,183 @@ def _log2_world(world: int) -> int:
     if world < 1 or world & (world - 1):
         raise ValueError(f"world size {world} is not a power of two")
     return world.bit_length() - 1
+
+
+class CsrShard:
+    """One rank's part of a row-partitioned CSR operator (host arrays).
+
+    rows [r0, r1) of the global matrix; `row_offsets` rebased to 0, `col`
+    renumbered: own column c -> c - r0, halo column -> n_local + its position
+    in `halo` (sorted by owner rank, then column).  `recv_counts[q]` halo
+    entries come from rank q; `send_idx[q]` are the local indices rank q
+    reads from this rank (in rank q's halo order)."""
+
+    __slots__ = ("rank", "r0", "r1", "row_offsets", "col", "values", "halo", "recv_counts", "send_idx")
+
+    def __init__(self, **kw):
+        for k, v in kw.items():
+            setattr(self, k, v)
+
+    @property
+    def n_local(self) -> int:
+        return self.r1 - self.r0
+
+    @property
+    def peers(self) -> list[int]:
+        """ranks exchanged with (either direction), ascending"""
+        return sorted({q for q, c in enumerate(self.recv_counts) if c} |
+                      {q for q, ix in enumerate(self.send_idx) if len(ix)})
+
+
+def csr_row_ranges(row_offsets: np.ndarray, world: int) -> list[tuple[int, int]]:
+    """Contiguous row ranges with about nnz / world entries each (every range
+    non-empty when there are at least `world` rows)."""
+    n = int(row_offsets.shape[0] - 1)
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    if n < world:
+        raise DimensionMismatch(f"{n} rows cannot be split over {world} ranks")
+    nnz = int(row_offsets[-1])
+    cuts = [0]
+    for r in range(1, world):
+        c = int(np.searchsorted(row_offsets, nnz * r / world, side="left"))
+        c = min(max(c, cuts[-1] + 1), n - (world - r))
+        cuts.append(c)
+    cuts.append(n)
+    return [(cuts[i], cuts[i + 1]) for i in range(world)]
+
+
+def csr_partition(row_offsets, col_indices, values, world: int) -> list[CsrShard]:
+    """Split a CSR matrix (square, global columns) row-wise over `world` ranks
+    with the halo lists of every rank."""
+    row_offsets = np.asarray(row_offsets, dtype=np.int64)
+    col_indices = np.asarray(col_indices, dtype=np.int64)
+    ranges = csr_row_ranges(row_offsets, world)
+    starts = np.array([r0 for r0, _ in ranges], dtype=np.int64)
+    owner_of = lambda cols: np.searchsorted(starts, cols, side="right") - 1   # noqa: E731
+    shards = []
+    for rank, (r0, r1) in enumerate(ranges):
+        lo, hi = int(row_offsets[r0]), int(row_offsets[r1])
+        cols = col_indices[lo:hi]
+        own = (cols >= r0) & (cols < r1)
+        ext = np.unique(cols[~own])                      # sorted global halo columns
+        owners = owner_of(ext)
+        order = np.lexsort((ext, owners))                # by owner rank, then column
+        halo, owners = ext[order], owners[order]
+        pos = np.empty(0, dtype=np.int64) if halo.size == 0 else None
+        local = np.empty(cols.shape[0], dtype=np.int64)
+        local[own] = cols[own] - r0
+        if halo.size:
+            # halo position of every remote column
+            sorter = np.argsort(halo)
+            pos = sorter[np.searchsorted(halo, cols[~own], sorter=sorter)]
+            local[~own] = (r1 - r0) + pos
+        recv_counts = np.bincount(owners, minlength=world).astype(np.int64)
+        shards.append(CsrShard(rank=rank, r0=r0, r1=r1,
+                               row_offsets=row_offsets[r0:r1 + 1] - lo, col=local,
+                               values=np.asarray(values)[lo:hi], halo=halo, recv_counts=recv_counts,
+                               send_idx=[None] * world))
+    # what each rank sends: the entries the others' halos list, in their order
+    for sh in shards:
+        offs = np.concatenate([[0], np.cumsum(sh.recv_counts)])
+        for q in range(world):
+            want = sh.halo[offs[q]:offs[q + 1]]
+            shards[q].send_idx[sh.rank] = (want - shards[q].r0).astype(np.int64)
+    for sh in shards:
+        sh.send_idx = [np.zeros(0, np.int64) if ix is None else ix for ix in sh.send_idx]
+    return shards
+
+
+class _DeviceCsrShard:
+    """A CsrShard on the device: local CSR (int32 renumbered columns), the
+    ping-pong extended vectors and the exchange lists."""
+
+    def __init__(self, engine: Engine, sh: CsrShard):
+        import torch
+        from .backend import DeviceCsr, to_device
+        self.engine, self.sh = engine, sh
+        n_ext = sh.n_local + len(sh.halo)
+        dev = engine.torch_device
+        self.csr = DeviceCsr(sh.n_local, n_ext, to_device(engine, sh.row_offsets),
+                             torch.from_numpy(sh.col.astype(np.int32)).to(dev),
+                             to_device(engine, np.ascontiguousarray(sh.values, dtype=np.complex128)))
+        self.x = empty_z(engine, max(1, n_ext))
+        self.y = empty_z(engine, max(1, n_ext))
+        self.peers = sh.peers
+        send = [sh.send_idx[q] for q in self.peers]
+        self.send_off = np.concatenate([[0], np.cumsum([len(i) for i in send])]).astype(np.int64)
+        rc = [int(sh.recv_counts[q]) for q in self.peers]
+        self.recv_off = np.concatenate([[0], np.cumsum(rc)]).astype(np.int64)
+        flat = np.concatenate(send) if send else np.zeros(0, np.int64)
+        self.send_idx = torch.from_numpy(flat.astype(np.int64)).to(dev) if flat.size else None
+        self.send_buf = empty_z(engine, max(1, int(self.send_off[-1])))
+
+    def step_local(self):
+        """y[:n_local] = local rows of U applied to x (halo already in place)."""
+        from .backend import spmv_device
+        spmv_device(self.engine, self.csr, self.x, self.y)
+        self.x, self.y = self.y, self.x
+
+
+class ShardedCsrWalk:
+    """This rank's rows of a coined walk on any graph (U built on the device,
+    partitioned by `csr_partition`), NCCL halo exchange per step.  For
+    lattices use SlabLattice (matrix-free).  Call collectively."""
+
+    def __init__(self, engine: Engine, spec, rank: int = 0, world: int = 1, group=None):
+        from . import coined as CO
+        self.engine, self.rank, self.world = engine, int(rank), int(world)
+        u = CO.device_operator(engine, spec.graph, spec.shift, spec.active_marked).to_host()
+        self.shards = csr_partition(u.row_offsets, u.col_indices, u.values, self.world)
+        self.local = _DeviceCsrShard(engine, self.shards[self.rank])
+        self.r0, self.r1 = self.local.sh.r0, self.local.sh.r1
+        if self.world > 1:
+            _init_comm(engine, self.rank, self.world, group)
+
+    def load(self, owned_arcs) -> None:
+        """owned_arcs: device tensor of this rank's arcs [r0, r1) (reference order)."""
+        self.local.x[: self.local.sh.n_local].copy_(owned_arcs)
+
+    def advance(self, steps: int) -> None:
+        L = self.local
+        peers = (C.c_int * max(1, len(L.peers)))(*L.peers)
+        for _ in range(int(steps)):
+            if self.world > 1:
+                self.engine.call("qwb_csr_halo_exchange", L.sh.n_local, N.ptr(L.x), N.ptr(L.send_idx),
+                                 L.send_off.ctypes.data_as(N._p_i64), L.recv_off.ctypes.data_as(N._p_i64),
+                                 peers, len(L.peers), N.ptr(L.send_buf), self.engine.stream())
+            L.step_local()
+
+    def store(self, owned_arcs) -> None:
+        owned_arcs.copy_(self.local.x[: self.local.sh.n_local])
+
+    def close(self) -> None:
+        if self.world > 1:
+            self.engine.call("qwb_comm_destroy")
+
+
+def emulate_csr_shards(engine: Engine, spec, world: int, psi: np.ndarray, steps: int) -> np.ndarray:
+    """The generic-graph row partition for `world` ranks on ONE device: the
+    halo lists are applied with device gathers in place of the NCCL group,
+    each shard stepped by the CSR kernel on its renumbered rows.  Returns the
+    full arc state.  Test hook for the multi-GPU generic-graph path."""
+    import torch
+    from . import coined as CO
+    u = CO.device_operator(engine, spec.graph, spec.shift, spec.active_marked).to_host()
+    shards = csr_partition(u.row_offsets, u.col_indices, u.values, world)
+    dev = [_DeviceCsrShard(engine, sh) for sh in shards]
+    full = torch.from_numpy(np.ascontiguousarray(psi, dtype=np.complex128)).to(engine.torch_device)
+    for d in dev:
+        d.x[: d.sh.n_local].copy_(full[d.sh.r0:d.sh.r1])
+    idx = [[torch.from_numpy(d.sh.send_idx[q]).to(engine.torch_device) for q in range(world)] for d in dev]
+    for _ in range(int(steps)):
+        for i, d in enumerate(dev):           # halo of shard i, ordered by owner rank
+            parts = [dev[q].x[idx[q][i]] for q in range(world) if d.sh.recv_counts[q]]
+            if parts:
+                d.x[d.sh.n_local: d.sh.n_local + len(d.sh.halo)].copy_(torch.cat(parts))
+        for d in dev:
+            d.step_local()
+    return torch.cat([d.x[: d.sh.n_local] for d in dev]).cpu().numpy()
 
 
 def _init_comm(engine: Engine, rank: int, world: int, group=None) -> None:

@@ -214,3 +214,76 @@ def test_gloo_multiprocess_hypercube_shards(tmp_path, world, marked):
     ref = O.evolve_state(O.hamiltonian(offs, cols, gamma, marked), _psi(1 << dim, dim), t, stats=stats)
     assert terms[0] == stats
     assert np.array_equal(got, ref)
+
+
+# ---------------------------------------------------------------------------
+# generic-graph CSR rows: contiguous nnz-balanced row ranges,
+# columns renumbered into [own | halo], per-step exchange of exactly the halo
+# entries (precomputed lists), then the local rows -- over gloo, vs the oracle
+# ---------------------------------------------------------------------------
+
+def _generic_u(n=120, seed=3):
+    rng = np.random.default_rng(seed)
+    edges = sorted({(min(a, b), max(a, b)) for a, b in rng.integers(0, n, size=(400, 2)) if a != b})
+    offs, cols = O.edges_adjacency(n, edges)
+    return O.evolution_operator(offs, cols, "flipflop", (5, 77))
+
+
+def test_csr_partition_plan():
+    u = _generic_u()
+    for world in (1, 2, 3, 7):
+        shards = DI.csr_partition(u.row_offsets, u.col_indices, u.values, world)
+        assert shards[0].r0 == 0 and shards[-1].r1 == u.n_rows
+        assert all(a.r1 == b.r0 for a, b in zip(shards, shards[1:]))
+        nnz = [int(s.row_offsets[-1]) for s in shards]
+        assert max(nnz) - min(nnz) <= 2 * int(np.diff(u.row_offsets).max()) + u.nnz // world // 4 + 4
+        x = _psi(u.n_rows, world)
+        ref = O.csr_rows(u, x, 0, u.n_rows)
+        got = []
+        for sh in shards:
+            xe = np.concatenate([x[sh.r0:sh.r1], x[sh.halo]])
+            got.append(O.csr_rows(O.Csr(sh.n_local, xe.size, sh.row_offsets, sh.col, sh.values), xe, 0, sh.n_local))
+            assert sh.rank not in sh.peers
+        assert np.array_equal(np.concatenate(got), ref)
+
+
+def _csr_worker(rank, world, port, steps, out_dir):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    u = _generic_u()
+    sh = DI.csr_partition(u.row_offsets, u.col_indices, u.values, world)[rank]
+    x = _psi(u.n_rows, 11)[sh.r0:sh.r1].copy()
+    m = O.Csr(sh.n_local, sh.n_local + len(sh.halo), sh.row_offsets, sh.col, sh.values)
+    offs = np.concatenate([[0], np.cumsum(sh.recv_counts)])
+    for _ in range(steps):
+        ops, recvs = [], {}
+        for q in sh.peers:       # same pairing as qwb_csr_halo_exchange's NCCL group
+            if len(sh.send_idx[q]):
+                ops.append(dist.P2POp(dist.isend, torch.from_numpy(x[sh.send_idx[q]].view(np.float64).copy()), q))
+            if sh.recv_counts[q]:
+                recvs[q] = torch.empty(2 * int(sh.recv_counts[q]), dtype=torch.float64)
+                ops.append(dist.P2POp(dist.irecv, recvs[q], q))
+        for r in (dist.batch_isend_irecv(ops) if ops else []):
+            r.wait()
+        xe = np.concatenate([x, np.zeros(len(sh.halo), complex)])
+        for q, t in recvs.items():
+            xe[sh.n_local + offs[q]: sh.n_local + offs[q + 1]] = t.numpy().view(np.complex128)
+        x = O.csr_rows(m, xe, 0, sh.n_local)
+    np.save(os.path.join(out_dir, f"csr{rank}.npy"), x)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_multiprocess_csr_halo(tmp_path, world):
+    import torch.multiprocessing as mp
+    port = _free_port()
+    mp.start_processes(_csr_worker, args=(world, port, 9, str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    got = np.concatenate([np.load(tmp_path / f"csr{r}.npy") for r in range(world)])
+    u = _generic_u()
+    ref = O.coined_simulate(u, _psi(u.n_rows, 11), [9])[0]
+    assert np.array_equal(got, ref)
