@@ -163,110 +163,6 @@ term_finalize_kernel(const double* __restrict__ partial, int nparts, double floo
 }
 
 // ---------------------------------------------------------------------------
-// Hypercube term, block-tiled (dim >= 9).  A CTA owns a 9-dim subcube of 512
-// consecutive vertices (bits 0..8), staged in shared memory; neighbours across
-// bits >= 9 are coalesced global loads (the same 512-B block for a whole warp),
-// prefetched into registers.  Row v's columns in ascending order are: v with
-// its set bits cleared from high to low, then v with its clear bits set from
-// low to high, so the reduction order is block-uniform for bits
-// >= 9, warp-uniform for bits 5..8, and only the 5 low bits permute per lane —
-// handled branch-free by computing that lane's bit for each of the 5 window
-// positions.  Warps holding a marked vertex (diagonal entry in the row) take
-// a per-lane generic path.
-// ---------------------------------------------------------------------------
-template <int MAXD>
-struct HcTile {
-  int dim;
-  double gamma;
-  const uint32_t* __restrict__ bits;
-};
-
-constexpr int kHcBlock = 512;
-
-template <int MAXD>
-__global__ void __launch_bounds__(kHcBlock, 1)
-hc_term_kernel(HcTile<MAXD> op, int64_t n, const double2* __restrict__ tin, double2* __restrict__ tout,
-               const double2* acc_in, double2* acc_out, double s_k, const int* __restrict__ done,
-               double* __restrict__ partial) {
-  if (*done) return;
-  __shared__ double2 seg[kHcBlock];
-  __shared__ double red[kHcBlock / 32];
-  const int tid = threadIdx.x;
-  const int dim = op.dim;
-  const double2 alpha = make_double2(0.0, -s_k);   // Python complex(-1j * tau / k)
-  const double2 one = make_double2(1.0, 0.0);
-  const double2 g = make_double2(-op.gamma, 0.0);
-  double nrm = 0.0;
-  for (int64_t base = (int64_t)blockIdx.x * kHcBlock; base < n; base += (int64_t)gridDim.x * kHcBlock) {
-    const int64_t v = base + tid;
-    double2 xs[MAXD];
-#pragma unroll
-    for (int b = 9; b < MAXD; ++b)
-      if (b < dim) xs[b] = __ldg(tin + (v ^ (1LL << b)));
-    const double2 xv = tin[v];
-    seg[tid] = xv;
-    __syncthreads();
-    const bool mk = op.bits && ((__ldg(op.bits + (v >> 5)) >> (v & 31)) & 1u);
-    double2 h;
-    if (__any_sync(0xffffffffu, mk)) {
-      StreamRow sr;
-      sr.init(dim + (mk ? 1 : 0));
-      for (int b = dim - 1; b >= 0; --b)
-        if ((v >> b) & 1) sr.push(cmul_np(g, __ldg(tin + (v ^ (1LL << b)))));
-      if (mk) sr.push(cmul_np(make_double2(-1.0, 0.0), xv));
-      for (int b = 0; b < dim; ++b)
-        if (!((v >> b) & 1)) sr.push(cmul_np(g, __ldg(tin + (v ^ (1LL << b)))));
-      h = sr.result();
-    } else {
-      StreamRow sr;
-      sr.init(dim);
-#pragma unroll
-      for (int b = MAXD - 1; b >= 9; --b)                  // set, high -> low (block-uniform)
-        if (b < dim && ((v >> b) & 1)) sr.push(cmul_np(g, xs[b]));
-#pragma unroll
-      for (int b = 8; b >= 5; --b)                         // set, warp-uniform
-        if ((v >> b) & 1) sr.push(cmul_np(g, seg[tid ^ (1 << b)]));
-      const unsigned low = (unsigned)(v & 31);
-      unsigned setm = low, clrm = (~low) & 31u;
-      const int pc = __popc(low);
-#pragma unroll
-      for (int q = 0; q < 5; ++q) {                        // 5 low bits: set desc, then clear asc
-        const int bs = 31 - __clz(setm | 1u);
-        const int bc = __ffs(clrm | 32u) - 1;
-        const bool use_set = q < pc;
-        const int b = use_set ? bs : bc;
-        setm = use_set ? (setm ^ (1u << bs)) : setm;
-        clrm = use_set ? clrm : (clrm ^ (1u << bc));
-        sr.push(cmul_np(g, seg[tid ^ (1 << b)]));
-      }
-#pragma unroll
-      for (int b = 5; b <= 8; ++b)                         // clear, warp-uniform
-        if (!((v >> b) & 1)) sr.push(cmul_np(g, seg[tid ^ (1 << b)]));
-#pragma unroll
-      for (int b = 9; b < MAXD; ++b)                       // clear, low -> high (block-uniform)
-        if (b < dim && !((v >> b) & 1)) sr.push(cmul_np(g, xs[b]));
-      h = sr.result();
-    }
-    const double2 t = cmul_np(alpha, h);
-    tout[v] = t;
-    acc_out[v] = cadd(acc_in[v], cmul_np(one, t));
-    nrm = __fma_rn(t.x, t.x, __fma_rn(t.y, t.y, nrm));
-    __syncthreads();   // seg is reused by the next subcube
-  }
-  // deterministic block reduction: warp butterflies, then warp 0 over 16 partials
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) nrm = __dadd_rn(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
-  if ((tid & 31) == 0) red[tid >> 5] = nrm;
-  __syncthreads();
-  if (tid < 32) {
-    double r = tid < kHcBlock / 32 ? red[tid] : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, o));
-    if (tid == 0) partial[blockIdx.x] = r;
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Hypercube term, positional form (dim >= 10).  The row's columns in ascending
 // order are v with its set bits cleared high->low, then v with its clear bits
 // set low->high.  The kernel walks the ROW POSITIONS p = 0..dim-1 at compile
@@ -772,13 +668,11 @@ void launch_stream(const HcStream& op, cudaStream_t s, int64_t n, const double2*
 
 int launch_term(const HcStream& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
                 const double2* ain, double2* acc, double s_k, const int* flags, double* partial) {
-  // QWB_HC_STREAM = CONS/256 * 10000 + NS * 100 + SPLIT (tuning knob)
+  // QWB_HC_STREAM = CONS/256 * 10000 + NS * 100 + SPLIT (tuning knob; measured at
+  // dim 22: 601 173, 20601 157, 20801 151-154 us/term)
   switch (op.variant) {
     case 601: launch_stream<6, 1, 256>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
-    case 1001: launch_stream<10, 1, 256>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
     case 20601: launch_stream<6, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
-    case 21001: launch_stream<10, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
-    case 21201: launch_stream<12, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
     default: launch_stream<8, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
   }
   return op.grid;
@@ -798,12 +692,6 @@ int launch_term(const Op& op, cudaStream_t s, int64_t n, const double2* tin, dou
   return kTermBlocks;
 }
 
-template <int MAXD>
-int launch_term(const HcTile<MAXD>& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
-                 const double2* ain, double2* acc, double s_k, const int* flags, double* partial) {
-  hc_term_kernel<MAXD><<<kTermBlocks, kHcBlock, 0, s>>>(op, n, tin, tout, ain, acc, s_k, flags, partial);
-  return kTermBlocks;
-}
 
 __global__ void apply_kernel_hc(HypercubeOp<32> op, int64_t n, const double2* __restrict__ x,
                                 double2* __restrict__ y) {
@@ -1091,7 +979,7 @@ int qwb_taylor_evolve_hypercube(qwb_ctx* ctx, int dim, double gamma, const uint3
   double2* w = reinterpret_cast<double2*>(work);
   cudaStream_t s = qwb::as_stream(stream);
   // QWB_HC_KERNEL: 3 = TMA-streamed tiles (default), 2 = positional gather,
-  // 1 = subcube tile, 0 = generic gather
+  // 0 = generic gather (the slower designs, kept for A/B measurements)
   static int tiled = -1;
   if (tiled < 0) {
     const char* e = getenv("QWB_HC_KERNEL");
@@ -1117,18 +1005,6 @@ int qwb_taylor_evolve_hypercube(qwb_ctx* ctx, int dim, double gamma, const uint3
       return evolve(ctx, op, n, p, w, substeps, tau, floor, max_terms, terms_host, s);
     }
     HcPos<31> op{dim, gamma, marked_bits};
-    return evolve(ctx, op, n, p, w, substeps, tau, floor, max_terms, terms_host, s);
-  }
-  if (tiled == 1) {
-    if (dim <= 16) {
-      HcTile<16> op{dim, gamma, marked_bits};
-      return evolve(ctx, op, n, p, w, substeps, tau, floor, max_terms, terms_host, s);
-    }
-    if (dim <= 24) {
-      HcTile<24> op{dim, gamma, marked_bits};
-      return evolve(ctx, op, n, p, w, substeps, tau, floor, max_terms, terms_host, s);
-    }
-    HcTile<32> op{dim, gamma, marked_bits};
     return evolve(ctx, op, n, p, w, substeps, tau, floor, max_terms, terms_host, s);
   }
   if (dim <= 16) {

@@ -12,7 +12,7 @@ cs = q.CtqwSpec(q.graphs.hypercube(dim), 1.0 / dim, 1.0, frozenset({0}))
 op = CT._Operator(eng, cs)
 n = 1 << dim
 x = torch.full((n,), 1.0 / np.sqrt(n), dtype=torch.complex128, device="cuda")
-for rep in range(2):
+for rep in range(4):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     terms = op.evolve(x, 1.0, 1e-12)
     torch.cuda.synchronize(); dt = time.perf_counter() - t0
