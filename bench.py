@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--walk-steps", type=int, default=1000)
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the multi-GPU (slab + NCCL) code path even on one rank (validation)")
     return ap.parse_args()
 
 
@@ -147,12 +149,22 @@ def dist_env():
     return rank, world, local
 
 
-def init_dist(world, backend):
+def init_dist(world, backend, force=False):
+    """torch.distributed for N > 1 (torchrun env); `force` also at N = 1
+    (--sharded: the multi-GPU code paths on one rank, for validation)."""
     import torch.distributed as dist
-    if world > 1 and not dist.is_initialized():
+    if (world > 1 or force) and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if world == 1:
+            import socket
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            os.environ.setdefault("MASTER_PORT", str(sk.getsockname()[1]))
+            sk.close()
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group(backend)
-    return dist if world > 1 else None
+    return dist if (world > 1 or force) else None
 
 
 def max_over_ranks(x: float, dist, device=None) -> float:
@@ -246,13 +258,14 @@ def run_b200(args):
     if world != args.gpus and world > 1:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
     torch.cuda.set_device(local)
-    dist = init_dist(world, "nccl")
+    dist = init_dist(world, "nccl", force=args.sharded)
     dev = torch.device("cuda", local)
+    single = world == 1 and not args.sharded
     eng = q.init_engine("b200", device=local)
 
     nx = args.nx
     walk = args.walk_steps
-    if world == 1:
+    if single:
         g = q.graphs.grid(nx, nx)
         spec = q.CoinedSpec(g)
         arcs = g.num_arcs
@@ -265,7 +278,7 @@ def run_b200(args):
     else:
         # weak scaling: one nx x (nx * world) torus, rank r owns rows [r*nx, (r+1)*nx)
         from paper_2406_08186_b200 import distributed as DI
-        runner = DI.SlabLattice(eng, nx, nx * world, "flipflop", (), rank, world)
+        runner = DI.SlabLattice(eng, nx, nx * world, "flipflop", (), rank, world, comm=True)
         arcs = 4 * nx * runner.rows
         rng = np.random.default_rng(rank)
         psi = rng.normal(size=arcs) + 1j * rng.normal(size=arcs)
@@ -305,14 +318,25 @@ def run_b200(args):
     from paper_2406_08186_b200 import _native as N
     dep, knd = C.c_int(0), C.c_int(0)
     N.load().qwb_lattice_fused_depth(nx, nx, 0, C.byref(dep), C.byref(knd))
-    depth = dep.value if world == 1 else 0
-    if depth > 0:
-        per_walk = walk // depth + walk % depth
-        kernel = (f"lattice_tb_kernel<flipflop, T={depth}, 32x48 region>" if knd.value == 1
-                  else f"lattice_wf_kernel<flipflop, T={depth}>")
+    if single:
+        depth = dep.value
+        if depth > 0:
+            per_walk = walk // depth + walk % depth
+            kernel = (f"lattice_tb_kernel<flipflop, T={depth}, 32x48 region>" if knd.value == 1
+                      else f"lattice_wf_kernel<flipflop, T={depth}>")
+        else:
+            per_walk = walk
+            kernel = "lattice_step_kernel<flipflop>"
+    elif runner.ghost:
+        # fused slabs: per G-step launch the middle band beside the ghost-row
+        # exchange, then the two edge bands; remainder steps one at a time
+        depth = runner.ghost
+        per_walk = 3 * (walk // depth) + walk % depth
+        kernel = f"lattice_tb_kernel<flipflop, T={depth}, 32x48 region> on y-slabs with {depth} ghost rows"
     else:
-        per_walk = walk * (1 if world == 1 else 2)
-        kernel = "lattice_step_kernel<flipflop>"
+        depth = 0
+        per_walk = 2 * walk
+        kernel = "lattice_step_kernel<flipflop> (slab boundary rows + interior rows)"
     launches = args.steps * per_walk
     step_s = el_ms / 1e3 / (args.steps * walk)          # per coined step (all rows)
     value = world * arcs * walk * args.steps / (el_ms / 1e3)
@@ -337,7 +361,7 @@ def run_b200(args):
             dist.barrier()
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        if world == 1:
+        if single:
             out = CO.simulate(eng, spec, (walk, walk + 1, 1), psi0)[0].amplitudes
         else:
             xd = q.backend.to_device(eng, host_local)
@@ -351,11 +375,11 @@ def run_b200(args):
             e2e_times.append(t1 - t0)
     e2e_s = max_over_ranks(sum(e2e_times), dist, dev)
     e2e_value = world * arcs * walk * len(e2e_times) / e2e_s
-    if world == 1:
+    if single:
         assert abs(np.linalg.norm(out) - 1.0) < 1e-9
 
     extras = {}
-    if not args.no_extras and world > 1:
+    if not args.no_extras and not single:
         try:
             c4 = measure_c4_sharded(q, dev, local, rank, world, dist)
         except Exception as e:  # pragma: no cover - reported, the headline line still prints
@@ -381,14 +405,15 @@ def run_b200(args):
             "config": {
                 "workload": (f"C2: grid {nx}x{nx} torus ({nx * nx} vertices, {arcs} arcs; BASELINE configs[1] "
                              f"'4M vertices, 16M arcs' per SURVEY D1), flip-flop Grover coin, {walk} coined "
-                             f"steps per bench step, matrix-free lattice kernel") if world == 1 else
+                             f"steps per bench step, matrix-free lattice kernel") if single else
                             (f"grid {nx}x{nx * world} torus split in {world} y-slabs of {nx}x{nx} "
                              f"({arcs} arcs per GPU), flip-flop Grover, {walk} coined steps per bench step, "
-                             f"NCCL halo exchange of 2 rows per step overlapped with interior rows"),
+                             f"temporally blocked slabs: NCCL exchange of {runner.ghost} ghost state rows per "
+                             f"plane and side every {runner.ghost} steps, overlapped with the middle band"),
                 "nx": nx, "ny": nx * world, "arcs": arcs * world, "coined_steps_per_bench_step": walk,
                 "psi0": "dense random complex128 (seeded per rank), normalised",
                 "l2": f"inputs larger than L2: 2 x {16 * arcs / 1e6:.0f} MB ping-pong state per GPU (> 126 MB L2)",
-                "parallelism": "dp1" if world == 1 else f"y-slab sharding over {world} GPUs (weak scaling)",
+                "parallelism": "dp1" if single else f"y-slab sharding over {world} GPUs (weak scaling)",
             },
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                          "frac": achieved_gbs / peak, "traffic": traffic,
@@ -408,7 +433,7 @@ def run_b200(args):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 16 * arcs,
                     "d2h_bytes_per_step": 16 * arcs,
-                    "call": "coined.simulate(engine, spec, (1000, 1001, 1), psi0) -> [WalkState]" if world == 1
+                    "call": "coined.simulate(engine, spec, (1000, 1001, 1), psi0) -> [WalkState]" if single
                     else "distributed.SlabLattice load(H2D pinned) + advance(1000) + store + D2H per rank",
                     "ms_per_call": e2e_s / len(e2e_times) * 1e3},
             "gpu_launches": launches,

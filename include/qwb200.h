@@ -181,6 +181,31 @@ int qwb_slab_probability(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64
 /* one step without exchange; part 0 = all owned rows, 1 = first+last, 2 = interior */
 int qwb_slab_step(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int shift,
                   const uint32_t* marked_bits, const qwb_z* in, qwb_z* out, int part, void* stream);
+/* Fused (temporally blocked) slabs: G = qwb_slab_ghost_rows(...) ghost rows
+ * each side (0: not available, use the 1-extra-row functions above); planes
+ * hold 4 x nx x (ny_local + 2G) qwb_z, owned rows are local rows [G, G+ny_local).
+ * qwb_slab_run_fused: G coined steps per launch of the temporally blocked kernel
+ * on the owned rows, preceded by an NCCL exchange of G state rows per plane
+ * with each y-neighbour; remainder steps one at a time (1-row exchange).  The
+ * same arithmetic as one GPU: bitwise equal.                                  */
+int qwb_slab_ghost_rows(int64_t nx, int64_t ny, int64_t ny_local, int64_t n_marked, int* ghost_host);
+int qwb_slab_to_planes_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
+                         const qwb_z* arcs, qwb_z* planes, void* stream);
+int qwb_slab_from_planes_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
+                           const qwb_z* planes, qwb_z* arcs, void* stream);
+int qwb_slab_probability_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
+                           const qwb_z* planes, double* p, void* stream);
+/* one launch without exchange: nsteps = ghost (temporally blocked) or 1 (pull step) */
+int qwb_slab_advance_local(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
+                           int shift, const uint32_t* marked_bits, const int64_t* marked_host, int64_t n_marked,
+                           const qwb_z* in, qwb_z* out, int nsteps, void* stream);
+int qwb_slab_run_fused(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
+                       int shift, const uint32_t* marked_bits, const int64_t* marked_host, int64_t n_marked,
+                       qwb_z* a, qwb_z* b, int64_t steps, int rank_below, int rank_above, int* final_in_b_host,
+                       void* stream);
+/* single-device emulation of the ghost-row exchange (g rows) between nslabs slabs (tests) */
+int qwb_slab_ghost_exchange_local(qwb_ctx* ctx, int64_t nx, int64_t ghost, int g, const int64_t* ny_local_host,
+                                  qwb_z* const* planes_host, int nslabs, void* stream);
 /* single-device emulation of the per-step exchange between nslabs slabs (tests) */
 int qwb_slab_exchange_local(qwb_ctx* ctx, int64_t nx, int shift, const int64_t* ny_local_host,
                             qwb_z* const* planes_host, int nslabs, void* stream);

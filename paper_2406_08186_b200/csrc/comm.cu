@@ -273,6 +273,123 @@ int qwb_csr_halo_exchange(qwb_ctx* ctx, int64_t n_local, qwb_z* x_ext, const int
   return qwb::nccl_sendrecv_list(ctx, sp, sc, rp, rc, peers_host, npeers, s);
 }
 
+// Ghost-row exchange of slab state (the fused multi-GPU lattice path): every
+// plane's first g owned rows go to the rank below's top ghost rows, the last
+// g owned rows to the rank above's bottom ghost rows (g = ghost before a
+// temporally blocked launch, 1 before a single pull step).
+static int ghost_exchange_nccl(qwb_ctx* ctx, int64_t nx, int64_t nl, int64_t G, int g, double2* planes,
+                               int below, int above, cudaStream_t s) {
+  NcclComm comm = (NcclComm)ctx->comm;
+  const int64_t P = nx * (nl + 2 * G);
+  const size_t cnt = 2 * (size_t)(g * nx);
+  QWB_NCCL(ctx, g_nccl.group_start());
+  for (int p = 0; p < 4; ++p) {
+    double2* pl = planes + p * P;
+    QWB_NCCL(ctx, g_nccl.send(pl + G * nx, cnt, kNcclFloat64, below, comm, s));
+    QWB_NCCL(ctx, g_nccl.recv(pl + (G + nl) * nx, cnt, kNcclFloat64, above, comm, s));
+    QWB_NCCL(ctx, g_nccl.send(pl + (G + nl - g) * nx, cnt, kNcclFloat64, above, comm, s));
+    QWB_NCCL(ctx, g_nccl.recv(pl + (G - g) * nx, cnt, kNcclFloat64, below, comm, s));
+  }
+  QWB_NCCL(ctx, g_nccl.group_end());
+  return QWB_OK;
+}
+
+// `steps` coined steps on a ghost-row slab: temporally blocked launches of
+// `ghost` steps each (ghost-row exchange before each), the remainder as
+// single pull steps (one-row exchange before each).  Result in a or b.
+int qwb_slab_run_fused(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
+                       int shift, const uint32_t* marked_bits, const int64_t* marked_host, int64_t n_marked,
+                       qwb_z* a, qwb_z* b, int64_t steps, int rank_below, int rank_above, int* final_in_b_host,
+                       void* stream) {
+  QWB_BEGIN(ctx);
+  if (!ctx->comm) QWB_FAIL(ctx, QWB_E_NCCL, "qwb_comm_init has not been called");
+  if (rank_below < 0 || rank_below >= ctx->nranks || rank_above < 0 || rank_above >= ctx->nranks)
+    QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "neighbour ranks out of range");
+  if (steps < 0) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "steps must be >= 0");
+  cudaStream_t s = qwb::as_stream(stream);
+  cudaStream_t cs = ctx->comm_stream;
+  double2* cur = reinterpret_cast<double2*>(a);
+  double2* nxt = reinterpret_cast<double2*>(b);
+  // Overlap: the temporally blocked launch is split into the band of tile
+  // rows that read no ghost row (owned rows [band, ny_local - band), launched
+  // while the ghost rows are in flight on the comm stream) and the two edge
+  // bands (after the exchange).  band = one tile row of owned rows.
+  const int band = qwb::lattice_tb_owned_rows((int)ghost);
+  static int split_env = -1;
+  if (split_env < 0) {
+    const char* e = getenv("QWB_SLAB_SPLIT");
+    split_env = (e && *e) ? atoi(e) : 1;
+  }
+  const bool split = split_env && band > 0 && ny_local >= 3 * (int64_t)band;
+  int swaps = 0;
+  for (int64_t k = 0; k < steps;) {
+    const int g = (k + ghost <= steps) ? (int)ghost : 1;
+    int st;
+    if (g == (int)ghost && split) {
+      QWB_CUDA(ctx, cudaEventRecord(ctx->ev_ready, s));
+      QWB_CUDA(ctx, cudaStreamWaitEvent(cs, ctx->ev_ready, 0));
+      st = ghost_exchange_nccl(ctx, nx, ny_local, ghost, g, cur, rank_below, rank_above, cs);
+      if (st) return st;
+      QWB_CUDA(ctx, cudaEventRecord(ctx->ev_done, cs));
+      const int lr = (int)(ny_local + 2 * ghost);
+      const qwb::TbGeo mid{lr, (int)ghost + band, (int)ny_local - 2 * band, (int)y0 + band, 0, 4};
+      st = qwb::lattice_tb_launch_geo(ctx, g, shift, s, (int)nx, (int)ny, mid, cur, nxt, marked_bits, marked_host,
+                                      n_marked);
+      if (st) return st;
+      QWB_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_done, 0));
+      const qwb::TbGeo lo{lr, (int)ghost, band, (int)y0, 0, 0};
+      const qwb::TbGeo hi{lr, (int)(ghost + ny_local) - band, band, (int)(y0 + ny_local) - band, 0, 0};
+      st = qwb::lattice_tb_launch_geo(ctx, g, shift, s, (int)nx, (int)ny, lo, cur, nxt, marked_bits, marked_host,
+                                      n_marked);
+      if (!st)
+        st = qwb::lattice_tb_launch_geo(ctx, g, shift, s, (int)nx, (int)ny, hi, cur, nxt, marked_bits,
+                                        marked_host, n_marked);
+      if (st) return st;
+      QWB_LAUNCH_CHECK(ctx, "lattice_tb_kernel(slab bands)");
+    } else {
+      st = ghost_exchange_nccl(ctx, nx, ny_local, ghost, g, cur, rank_below, rank_above, s);
+      if (st) return st;
+      st = qwb_slab_advance_local(ctx, nx, ny, y0, ny_local, ghost, shift, marked_bits, marked_host, n_marked,
+                                  reinterpret_cast<qwb_z*>(cur), reinterpret_cast<qwb_z*>(nxt), g, stream);
+      if (st) return st;
+    }
+    double2* t = cur;
+    cur = nxt;
+    nxt = t;
+    ++swaps;
+    k += g;
+  }
+  if (final_in_b_host) *final_in_b_host = swaps & 1;
+  return QWB_OK;
+}
+
+// the same exchange for nslabs ghost-row slabs on ONE device (tests)
+int qwb_slab_ghost_exchange_local(qwb_ctx* ctx, int64_t nx, int64_t ghost, int g, const int64_t* ny_local_host,
+                                  qwb_z* const* planes_host, int nslabs, void* stream) {
+  QWB_BEGIN(ctx);
+  if (g < 1 || g > ghost) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "exchange rows must be in 1..ghost");
+  cudaStream_t s = qwb::as_stream(stream);
+  const size_t bytes = 16 * (size_t)(g * nx);
+  for (int i = 0; i < nslabs; ++i) {
+    const int below = (i + nslabs - 1) % nslabs, above = (i + 1) % nslabs;
+    const int64_t nl = ny_local_host[i], P = nx * (nl + 2 * ghost);
+    const int64_t nlb = ny_local_host[below], Pb = nx * (nlb + 2 * ghost);
+    const int64_t nla = ny_local_host[above], Pa = nx * (nla + 2 * ghost);
+    double2* me = reinterpret_cast<double2*>(planes_host[i]);
+    double2* bl = reinterpret_cast<double2*>(planes_host[below]);
+    double2* ab = reinterpret_cast<double2*>(planes_host[above]);
+    for (int p = 0; p < 4; ++p) {
+      // my first g owned rows -> below's top ghost rows
+      QWB_CUDA(ctx, cudaMemcpyAsync(bl + p * Pb + (ghost + nlb) * nx, me + p * P + ghost * nx, bytes,
+                                    cudaMemcpyDeviceToDevice, s));
+      // my last g owned rows -> above's bottom ghost rows
+      QWB_CUDA(ctx, cudaMemcpyAsync(ab + p * Pa + (ghost - g) * nx, me + p * P + (ghost + nl - g) * nx, bytes,
+                                    cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  return QWB_OK;
+}
+
 // Single-process emulation of the exchange for P slabs held on ONE device
 // (tests): after qwb_slab_step(part=0) on every slab, move the two boundary
 // rows of slab i into its neighbours exactly as qwb_slab_run's NCCL group

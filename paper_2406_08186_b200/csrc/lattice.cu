@@ -68,8 +68,8 @@ __device__ __forceinline__ void slot_dirs(int x, int gy, int nx, int ny, int d[4
 }
 
 __device__ __forceinline__ int global_row(const Geom& g, int ly) {
-  int gy = g.gy0 + ly;
-  if (gy >= g.ny) gy -= g.ny;
+  int gy = g.gy0 + ly;   // >= 0; a whole-torus slab's ghost rows can wrap twice
+  while (gy >= g.ny) gy -= g.ny;
   return gy;
 }
 
@@ -269,6 +269,24 @@ int lattice_slab_geom(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t 
   return QWB_OK;
 }
 
+// slab with G ghost rows each side: owned rows are local rows [G, G + ny_local)
+int lattice_slab_geom_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
+                        Geom* g) {
+  int st = check_dims(ctx, nx, ny);
+  if (st) return st;
+  if (ghost < 1 || ghost > 8) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "ghost rows must be in 1..8");
+  if (ny_local < ghost || ny_local < 2 || y0 < 0 || y0 + ny_local > ny)
+    QWB_FAIL(ctx, QWB_E_DIMENSION, "slab rows [%lld, %lld) invalid for ny=%lld (need >= %lld rows)",
+             (long long)y0, (long long)(y0 + ny_local), (long long)ny, (long long)(ghost > 2 ? ghost : 2));
+  g->nx = (int)nx;
+  g->ny = (int)ny;
+  g->lrows = (int)(ny_local + 2 * ghost);
+  g->gy0 = (int)(((y0 - ghost) % ny + ny) % ny);
+  g->wrap = 0;
+  g->pstride = nx * (ny_local + 2 * ghost);
+  return QWB_OK;
+}
+
 Rows slab_rows(int64_t ny_local, int part) {
   const int nl = (int)ny_local;
   if (part == 1) return Rows{1, nl - 1, 2};
@@ -421,6 +439,82 @@ int qwb_slab_probability(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64
   lattice_prob_kernel<<<grid_for(g.nx, (int)ny_local), 256, 0, qwb::as_stream(stream)>>>(
       g, 1, (int)ny_local, reinterpret_cast<const double2*>(planes), p);
   QWB_LAUNCH_CHECK(ctx, "lattice_prob_kernel(slab)");
+  return QWB_OK;
+}
+
+int qwb_slab_to_planes_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
+                         const qwb_z* arcs, qwb_z* planes, void* stream) {
+  QWB_BEGIN(ctx);
+  Geom g;
+  int st = qwb::lattice_slab_geom_g(ctx, nx, ny, y0, ny_local, ghost, &g);
+  if (st) return st;
+  to_planes_kernel<<<grid_for(g.nx, (int)ny_local), 256, 0, qwb::as_stream(stream)>>>(
+      g, (int)ghost, (int)ny_local, reinterpret_cast<const double2*>(arcs), reinterpret_cast<double2*>(planes));
+  QWB_LAUNCH_CHECK(ctx, "to_planes_kernel(ghost slab)");
+  return QWB_OK;
+}
+
+int qwb_slab_from_planes_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
+                           const qwb_z* planes, qwb_z* arcs, void* stream) {
+  QWB_BEGIN(ctx);
+  Geom g;
+  int st = qwb::lattice_slab_geom_g(ctx, nx, ny, y0, ny_local, ghost, &g);
+  if (st) return st;
+  from_planes_kernel<<<grid_for(g.nx, (int)ny_local), 256, 0, qwb::as_stream(stream)>>>(
+      g, (int)ghost, (int)ny_local, reinterpret_cast<const double2*>(planes), reinterpret_cast<double2*>(arcs));
+  QWB_LAUNCH_CHECK(ctx, "from_planes_kernel(ghost slab)");
+  return QWB_OK;
+}
+
+int qwb_slab_probability_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
+                           const qwb_z* planes, double* p, void* stream) {
+  QWB_BEGIN(ctx);
+  Geom g;
+  int st = qwb::lattice_slab_geom_g(ctx, nx, ny, y0, ny_local, ghost, &g);
+  if (st) return st;
+  lattice_prob_kernel<<<grid_for(g.nx, (int)ny_local), 256, 0, qwb::as_stream(stream)>>>(
+      g, (int)ghost, (int)ny_local, reinterpret_cast<const double2*>(planes), p);
+  QWB_LAUNCH_CHECK(ctx, "lattice_prob_kernel(ghost slab)");
+  return QWB_OK;
+}
+
+int qwb_slab_ghost_rows(int64_t nx, int64_t ny, int64_t ny_local, int64_t n_marked, int* ghost_host) {
+  int d = qwb::lattice_kind() == 1 ? qwb::lattice_tb_depth(nx, ny, n_marked) : 0;
+  if (d < 2 || ny_local < d || nx < 64) d = 0;
+  if (ghost_host) *ghost_host = d;
+  return QWB_OK;
+}
+
+// One launch on a ghost-row slab, no exchange: nsteps == ghost runs the
+// temporally blocked kernel over the owned rows (reads the ghost rows' state),
+// nsteps == 1 one pull step (owned rows plus one ghost row each side pushed,
+// so every owned output receives all four pushes).
+int qwb_slab_advance_local(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
+                           int shift, const uint32_t* marked_bits, const int64_t* marked_host, int64_t n_marked,
+                           const qwb_z* in, qwb_z* out, int nsteps, void* stream) {
+  QWB_BEGIN(ctx);
+  Geom g;
+  int st = qwb::lattice_slab_geom_g(ctx, nx, ny, y0, ny_local, ghost, &g);
+  if (!st) st = qwb::lattice_check_shift(ctx, shift);
+  if (st) return st;
+  if (ghost < 2) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "ghost-row slabs need >= 2 ghost rows");
+  if (n_marked > 0 && (!marked_bits || !marked_host))
+    QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "marked vertices need both the bitmap and the host list");
+  cudaStream_t s = qwb::as_stream(stream);
+  const double2* x = reinterpret_cast<const double2*>(in);
+  double2* y = reinterpret_cast<double2*>(out);
+  if (nsteps == 1) {
+    TraceArgs tr{};
+    qwb::lattice_launch(shift, s, g, Rows{(int)ghost - 1, 1, (int)ny_local + 2}, x, y, marked_bits, nullptr, 0, tr);
+    QWB_LAUNCH_CHECK(ctx, "lattice_step_kernel(ghost slab)");
+    return QWB_OK;
+  }
+  if (nsteps != ghost) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "nsteps must be 1 or the ghost depth");
+  const qwb::TbGeo geo{(int)(ny_local + 2 * ghost), (int)ghost, (int)ny_local, (int)y0, 0, 0};
+  st = qwb::lattice_tb_launch_geo(ctx, (int)ghost, shift, s, (int)nx, (int)ny, geo, x, y, marked_bits,
+                                  marked_host, n_marked);
+  if (st) return st;
+  QWB_LAUNCH_CHECK(ctx, "lattice_tb_kernel(ghost slab)");
   return QWB_OK;
 }
 

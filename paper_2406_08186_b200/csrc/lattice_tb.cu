@@ -27,6 +27,8 @@
 
 namespace {
 
+using qwb::TbGeo;
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
@@ -160,7 +162,7 @@ struct MarkedList {   // up to 8 marked vertex ids; n < 0: more than 8 (use the 
 
 template <int SHIFT, bool MARKED, int T, int BY, int V, bool TRACE>
 __global__ void __launch_bounds__(32 * BY, 1)
-lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __restrict__ out,
+lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, double2* __restrict__ out,
                   const uint32_t* __restrict__ bits, MarkedList mk, TraceList tr, int tiles_x,
                   int ntiles) {
   using S = TbShape<BY, V>;
@@ -171,7 +173,7 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
   double2* xU = xD + 2 * S::NT;        // [2][BY][32] O_U of each thread's highest row
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * 32 + tx;
-  const int64_t n = (int64_t)nx * ny;
+  const int64_t n = (int64_t)nx * geo.lrows;   // plane stride of the buffers
 
   // tile coordinates advance by gridDim.x tiles per iteration: (gdiv, gmod)
   // rows / columns, carried without a division per tile
@@ -186,12 +188,15 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
   };
   auto prefetch = [&](double2* stage, int tcol, int trow) {
     const int bx = tcol * OX - T + tx;
-    const int by = trow * OY - T + ty * V;
+    const int by = geo.own0 + trow * OY - T + ty * V;   // local buffer row
     const int gx = wrapc(bx, nx);
 #pragma unroll
     for (int j = 0; j < V; ++j) {
-      const int gy = wrapc(by + j, ny);
-      const int64_t w = (int64_t)gy * nx + gx;
+      // rows outside a slab buffer are > T rows from every owned row: left stale
+      const int ly = by + j;
+      if (!geo.wrap && (ly < 0 || ly >= geo.lrows)) continue;
+      const int r = geo.wrap ? wrapc(ly, ny) : ly;
+      const int64_t w = (int64_t)r * nx + gx;
       const int li = (ty * V + j) * 32 + tx;
 #pragma unroll
       for (int p = 0; p < 4; ++p) cp_async16(stage + p * S::REG + li, in + p * n + w);
@@ -211,7 +216,10 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
   }
   for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
     double2* stage = stage0 + (size_t)(S::NSTAGE == 2 ? (it & 1) : 0) * 4 * S::REG;
-    const int x0 = tcol * OX, y0 = trow * OY;
+    // x0: global column of the tile's first owned column; y0: unwrapped
+    // global row of its first owned row; lyb: its local buffer row
+    const int x0 = tcol * OX, y0 = geo.ybase + trow * OY, lyb = geo.own0 + trow * OY;
+    const int trow_now = trow;
     advance(tcol, trow);
     const int gx = wrapc(x0 - T + tx, nx);
     int gy[V];
@@ -258,7 +266,7 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       const int ly = ty * V + j;
-      own[j] = col_ok && ly >= T && ly < T + OY && y0 + ly - T < ny;
+      own[j] = col_ok && ly >= T && ly < T + OY && trow_now * OY + ly - T < geo.nown;
     }
     if (interior)
       tile_steps<SHIFT, false, T, BY, V, true, false>(nx, ny, gx, gy, bits, vD, vL, vR, vU, xD, xU,
@@ -270,7 +278,7 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       if (own[j]) {
-        const int64_t w = (int64_t)gy[j] * nx + gx;
+        const int64_t w = (int64_t)(lyb - T + ty * V + j) * nx + gx;
         __stcs(out + w, make_double2(__dmul_rn(vD[j].x, kScale), __dmul_rn(vD[j].y, kScale)));
         __stcs(out + n + w, make_double2(__dmul_rn(vL[j].x, kScale), __dmul_rn(vL[j].y, kScale)));
         __stcs(out + 2 * n + w, make_double2(__dmul_rn(vR[j].x, kScale), __dmul_rn(vR[j].y, kScale)));
@@ -282,14 +290,15 @@ lattice_tb_kernel(int nx, int ny, const double2* __restrict__ in, double2* __res
 }
 
 template <int SHIFT, bool MARKED, int T, int BY, int V>
-int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const double2* in, double2* out,
-                const uint32_t* bits, const MarkedList& mk, const TraceList& tr) {
+int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const TbGeo& geo, const double2* in,
+                double2* out, const uint32_t* bits, const MarkedList& mk, const TraceList& tr) {
   using Sh = TbShape<BY, V>;
   constexpr int OX = Sh::RX - 2 * T, OY = Sh::RY - 2 * T;
-  const int tiles_x = (nx + OX - 1) / OX, tiles_y = (ny + OY - 1) / OY;
+  const int tiles_x = (nx + OX - 1) / OX, tiles_y = (geo.nown + OY - 1) / OY;
   const int ntiles = tiles_x * tiles_y;
   const size_t smem = Sh::smem_bytes();
-  const int grid = ntiles < ctx->num_sms ? ntiles : ctx->num_sms;
+  const int cap = ctx->num_sms - geo.spare_sms > 1 ? ctx->num_sms - geo.spare_sms : 1;
+  const int grid = ntiles < cap ? ntiles : cap;
   auto go = [&](auto kernel, bool* configured) -> int {
     const int dev = ctx->device & 255;
     if (!configured[dev]) {
@@ -297,7 +306,7 @@ int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const double2* in,
       if (e != cudaSuccess) return qwb::cuda_status(ctx, e, "cudaFuncSetAttribute(lattice_tb)");
       configured[dev] = true;
     }
-    kernel<<<grid, dim3(32, BY), smem, s>>>(nx, ny, in, out, bits, mk, tr, tiles_x, ntiles);
+    kernel<<<grid, dim3(32, BY), smem, s>>>(nx, ny, geo, in, out, bits, mk, tr, tiles_x, ntiles);
     return QWB_OK;
   };
   static bool conf_plain[256] = {}, conf_trace[256] = {};   // per instantiation and device
@@ -306,14 +315,14 @@ int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const double2* in,
 }
 
 template <int T, int BY, int V>
-int launch_tb(qwb_ctx* ctx, int shift, cudaStream_t s, int nx, int ny, const double2* in,
+int launch_tb(qwb_ctx* ctx, int shift, cudaStream_t s, int nx, int ny, const TbGeo& g, const double2* in,
               double2* out, const uint32_t* bits, const MarkedList& mk, const TraceList& tr) {
   if (shift == QWB_SHIFT_FLIPFLOP) {
-    return bits ? launch_tb_t<QWB_SHIFT_FLIPFLOP, true, T, BY, V>(ctx, s, nx, ny, in, out, bits, mk, tr)
-                : launch_tb_t<QWB_SHIFT_FLIPFLOP, false, T, BY, V>(ctx, s, nx, ny, in, out, bits, mk, tr);
+    return bits ? launch_tb_t<QWB_SHIFT_FLIPFLOP, true, T, BY, V>(ctx, s, nx, ny, g, in, out, bits, mk, tr)
+                : launch_tb_t<QWB_SHIFT_FLIPFLOP, false, T, BY, V>(ctx, s, nx, ny, g, in, out, bits, mk, tr);
   }
-  return bits ? launch_tb_t<QWB_SHIFT_PERSISTENT, true, T, BY, V>(ctx, s, nx, ny, in, out, bits, mk, tr)
-              : launch_tb_t<QWB_SHIFT_PERSISTENT, false, T, BY, V>(ctx, s, nx, ny, in, out, bits, mk, tr);
+  return bits ? launch_tb_t<QWB_SHIFT_PERSISTENT, true, T, BY, V>(ctx, s, nx, ny, g, in, out, bits, mk, tr)
+              : launch_tb_t<QWB_SHIFT_PERSISTENT, false, T, BY, V>(ctx, s, nx, ny, g, in, out, bits, mk, tr);
 }
 
 int env_int(const char* name, int dflt) {
@@ -475,11 +484,11 @@ int lattice_tb_depth(int64_t nx, int64_t ny, int64_t n_marked) {
   return depth;
 }
 
-int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny,
-                      const double2* in, double2* out, const uint32_t* bits,
-                      const int64_t* marked_host, int64_t n_marked,
-                      const int64_t* trace_vertices_host, int n_trace, double* trace) {
+static int tb_launch_impl(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny, const TbGeo& geo,
+                          const double2* in, double2* out, const uint32_t* bits, const int64_t* marked_host,
+                          int64_t n_marked, const int64_t* trace_vertices_host, int n_trace, double* trace) {
   if (lattice_kind() == 0) {
+    if (!geo.wrap) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "the wavefront kernel does not run on slabs");
     if (trace) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "the wavefront kernel does not fuse traces");
     MarkedList mk{};
     mk.n = (int)n_marked;
@@ -517,9 +526,9 @@ int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx
   // each (32x48 region); 3: 32x16 threads, 3 rows each (32x48 region)
 #define QWB_TB_CASE(T_)                                                                        \
   case T_:                                                                                     \
-    if (shape == 2) return launch_tb<T_, 24, 2>(ctx, shift, s, nx, ny, in, out, bits, mk, tl); \
-    if (shape == 3) return launch_tb<T_, 16, 3>(ctx, shift, s, nx, ny, in, out, bits, mk, tl); \
-    return launch_tb<T_, 16, 2>(ctx, shift, s, nx, ny, in, out, bits, mk, tl);
+    if (shape == 2) return launch_tb<T_, 24, 2>(ctx, shift, s, nx, ny, geo, in, out, bits, mk, tl); \
+    if (shape == 3) return launch_tb<T_, 16, 3>(ctx, shift, s, nx, ny, geo, in, out, bits, mk, tl); \
+    return launch_tb<T_, 16, 2>(ctx, shift, s, nx, ny, geo, in, out, bits, mk, tl);
   switch (depth) {
     QWB_TB_CASE(2)
     QWB_TB_CASE(3)
@@ -530,6 +539,29 @@ int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx
       QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "unsupported temporal block depth %d", depth);
   }
 #undef QWB_TB_CASE
+}
+
+int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny,
+                      const double2* in, double2* out, const uint32_t* bits,
+                      const int64_t* marked_host, int64_t n_marked,
+                      const int64_t* trace_vertices_host, int n_trace, double* trace) {
+  const TbGeo geo{ny, 0, ny, 0, 1, 0};
+  return tb_launch_impl(ctx, depth, shift, s, nx, ny, geo, in, out, bits, marked_host, n_marked,
+                        trace_vertices_host, n_trace, trace);
+}
+
+int lattice_tb_owned_rows(int depth) {
+  if (lattice_kind() != 1 || depth < 2) return 0;
+  const int shape = env_int("QWB_LATTICE_SHAPE", 3);
+  const int ry = shape == 2 ? 24 * 2 : shape == 3 ? 16 * 3 : 16 * 2;
+  return ry - 2 * (depth > 6 ? 6 : depth);
+}
+
+int lattice_tb_launch_geo(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny, const TbGeo& geo,
+                          const double2* in, double2* out, const uint32_t* bits, const int64_t* marked_host,
+                          int64_t n_marked) {
+  return tb_launch_impl(ctx, depth, shift, s, nx, ny, geo, in, out, bits, marked_host, n_marked, nullptr, 0,
+                        nullptr);
 }
 
 }  // namespace qwb

@@ -225,14 +225,28 @@ void lattice_launch(int shift, cudaStream_t s, const Geom& g, const Rows& r, con
                     double2* out, const uint32_t* bits, double* prob, int prob_row0,
                     const TraceArgs& tr);
 int lattice_check_shift(qwb_ctx* ctx, int shift);
-// temporally blocked single-GPU torus steps (lattice_tb.cu)
+// temporally blocked torus steps (lattice_tb.cu).  TbGeo: the rows a launch
+// owns inside a planes buffer of lrows rows (plane stride nx * lrows): local
+// rows [own0, own0 + nown) = global rows [ybase, ybase + nown).  wrap = 1:
+// the buffer is the whole torus (rows wrap inside it); wrap = 0: a slab with
+// >= T ghost rows each side holding the neighbours' state (no wrap).
+struct TbGeo {
+  int lrows, own0, nown, ybase, wrap;
+  int spare_sms;   // SMs left free (for NCCL kernels running alongside)
+};
 int lattice_tb_depth(int64_t nx, int64_t ny, int64_t n_marked);
 int lattice_kind();   // 1 = CTA-tile kernel, 0 = wavefront kernel
+int lattice_tb_owned_rows(int depth);   // owned rows per tile row of the tile kernel (0: n/a)
+int lattice_tb_launch_geo(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny, const TbGeo& geo,
+                          const double2* in, double2* out, const uint32_t* bits, const int64_t* marked_host,
+                          int64_t n_marked);
 int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny,
                       const double2* in, double2* out, const uint32_t* bits,
                       const int64_t* marked_host, int64_t n_marked,
                       const int64_t* trace_vertices_host, int n_trace, double* trace);
 int lattice_slab_geom(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, Geom* g);
+int lattice_slab_geom_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
+                        Geom* g);
 // part: 0 = all owned rows, 1 = first and last owned rows, 2 = interior owned rows
 Rows slab_rows(int64_t ny_local, int part);
 

@@ -223,14 +223,16 @@ class ShardedCsrWalk:
     partitioned by `csr_partition`), NCCL halo exchange per step.  For
     lattices use SlabLattice (matrix-free).  Call collectively."""
 
-    def __init__(self, engine: Engine, spec, rank: int = 0, world: int = 1, group=None):
+    def __init__(self, engine: Engine, spec, rank: int = 0, world: int = 1, group=None,
+                 comm: bool | None = None):
         from . import coined as CO
         self.engine, self.rank, self.world = engine, int(rank), int(world)
+        self.comm = self.world > 1 if comm is None else bool(comm)
         u = CO.device_operator(engine, spec.graph, spec.shift, spec.active_marked).to_host()
         self.shards = csr_partition(u.row_offsets, u.col_indices, u.values, self.world)
         self.local = _DeviceCsrShard(engine, self.shards[self.rank])
         self.r0, self.r1 = self.local.sh.r0, self.local.sh.r1
-        if self.world > 1:
+        if self.comm:
             _init_comm(engine, self.rank, self.world, group)
 
     def load(self, owned_arcs) -> None:
@@ -241,7 +243,7 @@ class ShardedCsrWalk:
         L = self.local
         peers = (C.c_int * max(1, len(L.peers)))(*L.peers)
         for _ in range(int(steps)):
-            if self.world > 1:
+            if self.comm:
                 self.engine.call("qwb_csr_halo_exchange", L.sh.n_local, N.ptr(L.x), N.ptr(L.send_idx),
                                  L.send_off.ctypes.data_as(N._p_i64), L.recv_off.ctypes.data_as(N._p_i64),
                                  peers, len(L.peers), N.ptr(L.send_buf), self.engine.stream())
@@ -251,7 +253,7 @@ class ShardedCsrWalk:
         owned_arcs.copy_(self.local.x[: self.local.sh.n_local])
 
     def close(self) -> None:
-        if self.world > 1:
+        if self.comm:
             self.engine.call("qwb_comm_destroy")
 
 
@@ -318,17 +320,18 @@ class ShardedHypercubeWalk:
     H = -gamma A - sum_M |v><v| (ctqw.py:84-98).  Call collectively."""
 
     def __init__(self, engine: Engine, dim: int, gamma: float, marked=(), rank: int = 0, world: int = 1,
-                 group=None):
+                 group=None, comm: bool | None = None):
         self.engine = engine
         self.dim, self.gamma = int(dim), float(gamma)
         self.rank, self.world = int(rank), int(world)
+        self.comm = self.world > 1 if comm is None else bool(comm)
         self.S = _log2_world(self.world)
         self.lo, self.hi = hypercube_shard(self.dim, self.world, self.rank)
         self.n_local = self.hi - self.lo
         self.group = group
         self.bits, self.inf_norm = _hypercube_setup(engine, self.dim, self.gamma, marked)
         self.work = empty_z(engine, (3 + self.S) * self.n_local)
-        if self.world > 1:
+        if self.comm:
             _init_comm(engine, self.rank, self.world, group)
 
     def global_norm(self, psi_local) -> float:
@@ -352,7 +355,7 @@ class ShardedHypercubeWalk:
         floor = tol * self.global_norm(psi_local)
         terms = (C.c_int * substeps)()
         eng = self.engine
-        if self.world == 1:
+        if not self.comm:
             eng.call("qwb_taylor_evolve_hypercube", self.dim, self.gamma, N.ptr(self.bits), N.ptr(psi_local),
                      N.ptr(self.work), substeps, tau, floor, int(CT._MAX_SERIES_TERMS), terms, eng.stream())
         else:
@@ -362,7 +365,7 @@ class ShardedHypercubeWalk:
         return list(terms)
 
     def close(self) -> None:
-        if self.world > 1:
+        if self.comm:
             self.engine.call("qwb_comm_destroy")
 
 
@@ -395,57 +398,142 @@ class SlabLattice:
     persistent shift, optional marked vertices).  Call collectively."""
 
     def __init__(self, engine: Engine, nx: int, ny: int, shift: str = "flipflop", marked=(),
-                 rank: int = 0, world: int = 1, group=None):
+                 rank: int = 0, world: int = 1, group=None, comm: bool | None = None):
         import torch
         self.engine = engine
         self.nx, self.ny = int(nx), int(ny)
         self.rank, self.world = int(rank), int(world)
+        # comm: run through the NCCL exchange (default when world > 1; with
+        # world == 1 the single slab exchanges with itself = the torus wrap)
+        self.comm = self.world > 1 if comm is None else bool(comm)
         self.y0, self.rows = slab_partition(self.ny, self.world)[self.rank]
         self.below, self.above = neighbours(self.rank, self.world)
         self.shift = N.SHIFT[shift]
         self.bits = None
+        self.marked = sorted(int(v) for v in marked)
+        self.marked_arr = N.i64_array(self.marked)
         if marked:
             n = self.nx * self.ny
             self.bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=engine.torch_device)
-            mk = torch.tensor(sorted(int(v) for v in marked), dtype=torch.int64, device=engine.torch_device)
+            mk = torch.tensor(self.marked, dtype=torch.int64, device=engine.torch_device)
             engine.call("qwb_marked_bitmap", n, N.ptr(mk), len(marked), N.ptr(self.bits), engine.stream())
-        size = 4 * self.nx * (self.rows + 2)
+        # fused path: G ghost state rows each side, G steps per temporally
+        # blocked launch (the same G on every rank: from the smallest slab)
+        self.ghost = slab_ghost_rows(self.nx, self.ny, self.world, len(self.marked))
+        size = 4 * self.nx * (self.rows + 2 * (self.ghost or 1))
         self.a = empty_z(engine, size)
         self.b = empty_z(engine, size)
         self.a.zero_()
         self.b.zero_()
-        if self.world > 1:
+        if self.comm:
             _init_comm(engine, self.rank, self.world, group)
 
     def load(self, owned_arcs) -> None:
         """owned_arcs: device tensor of this slab's arcs (reference order)."""
-        self.engine.call("qwb_slab_to_planes", self.nx, self.ny, self.y0, self.rows, N.ptr(owned_arcs),
-                         N.ptr(self.a), self.engine.stream())
+        if self.ghost:
+            self.engine.call("qwb_slab_to_planes_g", self.nx, self.ny, self.y0, self.rows, self.ghost,
+                             N.ptr(owned_arcs), N.ptr(self.a), self.engine.stream())
+        else:
+            self.engine.call("qwb_slab_to_planes", self.nx, self.ny, self.y0, self.rows, N.ptr(owned_arcs),
+                             N.ptr(self.a), self.engine.stream())
 
     def advance(self, steps: int) -> None:
         if steps <= 0:
             return
         eng = self.engine
-        if self.world == 1:
-            raise RuntimeError("use the single-GPU lattice path for world == 1")
+        if not self.comm:
+            raise RuntimeError("use the single-GPU lattice path for world == 1 (or comm=True)")
         flag = C.c_int(0)
-        eng.call("qwb_slab_run", self.nx, self.ny, self.y0, self.rows, self.shift, N.ptr(self.bits),
-                 N.ptr(self.a), N.ptr(self.b), int(steps), self.below, self.above, C.byref(flag),
-                 eng.stream())
+        if self.ghost:
+            eng.call("qwb_slab_run_fused", self.nx, self.ny, self.y0, self.rows, self.ghost, self.shift,
+                     N.ptr(self.bits), self.marked_arr, len(self.marked), N.ptr(self.a), N.ptr(self.b), int(steps),
+                     self.below, self.above, C.byref(flag), eng.stream())
+        else:
+            eng.call("qwb_slab_run", self.nx, self.ny, self.y0, self.rows, self.shift, N.ptr(self.bits),
+                     N.ptr(self.a), N.ptr(self.b), int(steps), self.below, self.above, C.byref(flag),
+                     eng.stream())
         if flag.value:
             self.a, self.b = self.b, self.a
 
     def store(self, owned_arcs) -> None:
-        self.engine.call("qwb_slab_from_planes", self.nx, self.ny, self.y0, self.rows, N.ptr(self.a),
-                         N.ptr(owned_arcs), self.engine.stream())
+        if self.ghost:
+            self.engine.call("qwb_slab_from_planes_g", self.nx, self.ny, self.y0, self.rows, self.ghost,
+                             N.ptr(self.a), N.ptr(owned_arcs), self.engine.stream())
+        else:
+            self.engine.call("qwb_slab_from_planes", self.nx, self.ny, self.y0, self.rows, N.ptr(self.a),
+                             N.ptr(owned_arcs), self.engine.stream())
 
     def probability(self, p) -> None:
-        self.engine.call("qwb_slab_probability", self.nx, self.ny, self.y0, self.rows, N.ptr(self.a),
-                         N.ptr(p), self.engine.stream())
+        if self.ghost:
+            self.engine.call("qwb_slab_probability_g", self.nx, self.ny, self.y0, self.rows, self.ghost,
+                             N.ptr(self.a), N.ptr(p), self.engine.stream())
+        else:
+            self.engine.call("qwb_slab_probability", self.nx, self.ny, self.y0, self.rows, N.ptr(self.a),
+                             N.ptr(p), self.engine.stream())
 
     def close(self) -> None:
-        if self.world > 1:
+        if self.comm:
             self.engine.call("qwb_comm_destroy")
+
+
+def slab_ghost_rows(nx: int, ny: int, world: int, n_marked: int) -> int:
+    """Ghost rows G of the fused (temporally blocked) slab path, 0 when it is
+    not available (tiny lattices, slabs thinner than G rows, or
+    QWB_SLAB_FUSED=0).  Identical on every rank."""
+    if os.environ.get("QWB_SLAB_FUSED", "1") == "0":
+        return 0
+    min_rows = min(r for _, r in slab_partition(ny, world))
+    g = C.c_int(0)
+    N.check(N.load().qwb_slab_ghost_rows(nx, ny, min_rows, n_marked, C.byref(g)))
+    return int(g.value)
+
+
+def emulate_slabs_fused(engine: Engine, nx: int, ny: int, world: int, psi_arcs: np.ndarray, steps: int,
+                        shift: str = "flipflop", marked=()):
+    """The fused slab decomposition (G ghost state rows, G steps per
+    temporally blocked launch, single pull steps for the remainder) for
+    `world` slabs on ONE device, exchanging ghost rows with device copies
+    exactly as qwb_slab_run_fused's NCCL group does.  Returns the full arc
+    state.  Test hook for the multi-GPU path."""
+    import torch
+    parts = slab_partition(ny, world)
+    sh = N.SHIFT[shift]
+    marked = sorted(int(v) for v in marked)
+    G = slab_ghost_rows(nx, ny, world, len(marked))
+    if G == 0:
+        raise ValueError("the fused slab path is not available for this lattice")
+    bits = None
+    if marked:
+        n = nx * ny
+        bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=engine.torch_device)
+        mk = torch.tensor(marked, dtype=torch.int64, device=engine.torch_device)
+        engine.call("qwb_marked_bitmap", n, N.ptr(mk), len(marked), N.ptr(bits), engine.stream())
+    marr = N.i64_array(marked)
+    full = torch.from_numpy(np.ascontiguousarray(psi_arcs)).to(engine.torch_device)
+    cur, nxt = [], []
+    for (y0, rows) in parts:
+        a = empty_z(engine, 4 * nx * (rows + 2 * G)).zero_()
+        b = empty_z(engine, 4 * nx * (rows + 2 * G)).zero_()
+        lo, hi = owned_arc_range(nx, y0, rows)
+        engine.call("qwb_slab_to_planes_g", nx, ny, y0, rows, G, N.ptr(full[lo:hi]), N.ptr(a), engine.stream())
+        cur.append(a)
+        nxt.append(b)
+    nl = N.i64_array([r for (_, r) in parts])
+    k = 0
+    while k < steps:
+        g = G if k + G <= steps else 1
+        ptrs = (C.c_void_p * world)(*[N.ptr(t) for t in cur])
+        engine.call("qwb_slab_ghost_exchange_local", nx, G, g, nl, ptrs, world, engine.stream())
+        for i, (y0, rows) in enumerate(parts):
+            engine.call("qwb_slab_advance_local", nx, ny, y0, rows, G, sh, N.ptr(bits), marr, len(marked),
+                        N.ptr(cur[i]), N.ptr(nxt[i]), g, engine.stream())
+        cur, nxt = nxt, cur
+        k += g
+    out = torch.empty_like(full)
+    for i, (y0, rows) in enumerate(parts):
+        lo, hi = owned_arc_range(nx, y0, rows)
+        engine.call("qwb_slab_from_planes_g", nx, ny, y0, rows, G, N.ptr(cur[i]), N.ptr(out[lo:hi]), engine.stream())
+    return out.cpu().numpy()
 
 
 def emulate_slabs(engine: Engine, nx: int, ny: int, world: int, psi_arcs: np.ndarray, steps: int,
