@@ -123,3 +123,36 @@ def run_full(nx, ny, arcs, steps, shift="flipflop", marked=()):
         planes = step_slab(nx, ny, 0, ny, planes, shift, marked)
         exchange_local([planes], shift)
     return planes_to_arcs(nx, ny, planes, extra=1)
+
+
+# ---- fused (ghost-row) slabs: csrc/comm.cu qwb_slab_run_fused ------------------
+
+def ghost_window(nx, ny, arcs_owned, y0, rows, G):
+    """Planes (4, rows + 2G, nx) of a slab with G ghost state rows each side
+    (ghosts zero until the first exchange)."""
+    w = np.zeros((4, rows + 2 * G, nx), dtype=np.complex128)
+    w[:, G:G + rows, :] = arcs_to_planes(nx, ny, arcs_owned, y0, rows)
+    return w
+
+
+def ghost_steps(nx, ny, y0, rows, G, window, steps, shift="flipflop", marked=()):
+    """`steps` (<= G) steps on the window with open y boundaries: after them
+    the owned rows are exact (each step spoils one more window row per side)."""
+    for _ in range(steps):
+        padded = np.zeros((4, rows + 2 * G + 2, nx), dtype=np.complex128)
+        padded[:, 1:-1, :] = window
+        out = step_slab(nx, ny, y0 - G, rows + 2 * G, padded, shift, marked)
+        window = out[:, 1:-1, :]
+    return window
+
+
+def ghost_sends(window, rows, G, g):
+    """(rows for the rank below, rows for the rank above): the first / last g
+    owned rows of every plane."""
+    return window[:, G:G + g, :].copy(), window[:, G + rows - g:G + rows, :].copy()
+
+
+def ghost_receive(window, rows, G, g, from_above, from_below):
+    window[:, G + rows:G + rows + g, :] = from_above     # top ghost rows
+    window[:, G - g:G, :] = from_below                   # bottom ghost rows
+    return window

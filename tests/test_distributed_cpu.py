@@ -287,3 +287,51 @@ def test_gloo_multiprocess_csr_halo(tmp_path, world):
     u = _generic_u()
     ref = O.coined_simulate(u, _psi(u.n_rows, 11), [9])[0]
     assert np.array_equal(got, ref)
+
+
+# ---------------------------------------------------------------------------
+# fused lattice slabs (qwb_slab_run_fused): G ghost state rows each side, G
+# steps per exchange (single steps for the remainder), over gloo, vs the oracle
+# ---------------------------------------------------------------------------
+
+def _ghost_worker(rank, world, port, nx, ny, G, steps, shift, marked, out_dir):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    psi = _psi(4 * nx * ny, 21)
+    y0, rows = DI.slab_partition(ny, world)[rank]
+    below, above = DI.neighbours(rank, world)
+    lo, hi = DI.owned_arc_range(nx, y0, rows)
+    win = PM.ghost_window(nx, ny, psi[lo:hi], y0, rows, G)
+    k = 0
+    while k < steps:
+        g = G if k + G <= steps else 1
+        down, up = PM.ghost_sends(win, rows, G, g)
+        from_above = torch.empty(down.shape, dtype=torch.complex128)
+        from_below = torch.empty(up.shape, dtype=torch.complex128)
+        # comm.cu's pairing: send down / recv from above / send up / recv from below
+        ops = [dist.P2POp(dist.isend, torch.from_numpy(down), below), dist.P2POp(dist.irecv, from_above, above),
+               dist.P2POp(dist.isend, torch.from_numpy(up), above), dist.P2POp(dist.irecv, from_below, below)]
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+        win = PM.ghost_receive(win, rows, G, g, from_above.numpy(), from_below.numpy())
+        win = PM.ghost_steps(nx, ny, y0, rows, G, win, g, shift, marked)
+        k += g
+    np.save(os.path.join(out_dir, f"ghost{rank}.npy"), PM.planes_to_arcs(nx, ny, win, y0, rows, extra=G))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,G,shift", [(2, 4, "flipflop"), (3, 3, "persistent"), (2, 2, "flipflop")])
+def test_gloo_multiprocess_ghost_slabs(tmp_path, world, G, shift):
+    import torch.multiprocessing as mp
+    nx, ny, steps, marked = 8, 18, 11, (17, 100)
+    port = _free_port()
+    mp.start_processes(_ghost_worker, args=(world, port, nx, ny, G, steps, shift, marked, str(tmp_path)),
+                       nprocs=world, join=True, start_method="spawn")
+    got = np.concatenate([np.load(tmp_path / f"ghost{r}.npy") for r in range(world)])
+    offs, cols = O.grid_adjacency(nx, ny)
+    u = O.evolution_operator(offs, cols, shift, marked, "grid", (nx, ny, True))
+    assert np.array_equal(got, O.coined_simulate(u, _psi(4 * nx * ny, 21), [steps])[0])
