@@ -479,7 +479,7 @@ int qwb_slab_probability_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int
 }
 
 int qwb_slab_ghost_rows(int64_t nx, int64_t ny, int64_t ny_local, int64_t n_marked, int* ghost_host) {
-  int d = qwb::lattice_kind() == 1 ? qwb::lattice_tb_depth(nx, ny, n_marked) : 0;
+  int d = qwb::lattice_slab_depth(qwb::lattice_tb_depth(nx, ny, n_marked));
   if (d < 2 || ny_local < d || nx < 64) d = 0;
   if (ghost_host) *ghost_host = d;
   return QWB_OK;

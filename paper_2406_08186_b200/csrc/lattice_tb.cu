@@ -48,6 +48,8 @@ __device__ __forceinline__ double2 shfl_up2(double2 v) {
   return make_double2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
 }
 
+constexpr int kSlabDepth = 4;   // the slab (ghost-row) kernels are built for this depth
+
 template <int BY, int V>
 struct TbShape {
   static constexpr int RX = 32;            // region columns (= warp lanes)
@@ -160,7 +162,8 @@ struct MarkedList {   // up to 8 marked vertex ids; n < 0: more than 8 (use the 
   int x[8], y[8];     // their coordinates (host-computed)
 };
 
-template <int SHIFT, bool MARKED, int T, int BY, int V, bool TRACE>
+// SLAB: the buffer is a y-slab with ghost rows (geo), else the whole torus
+template <int SHIFT, bool MARKED, int T, int BY, int V, bool TRACE, bool SLAB>
 __global__ void __launch_bounds__(32 * BY, 1)
 lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, double2* __restrict__ out,
                   const uint32_t* __restrict__ bits, MarkedList mk, TraceList tr, int tiles_x,
@@ -173,6 +176,7 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
   double2* xU = xD + 2 * S::NT;        // [2][BY][32] O_U of each thread's highest row
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * 32 + tx;
+  if (!SLAB) geo = TbGeo{ny, 0, ny, 0, 1, 0};   // compile-time constants for the torus
   const int64_t n = (int64_t)nx * geo.lrows;   // plane stride of the buffers
 
   // tile coordinates advance by gridDim.x tiles per iteration: (gdiv, gmod)
@@ -194,8 +198,8 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
     for (int j = 0; j < V; ++j) {
       // rows outside a slab buffer are > T rows from every owned row: left stale
       const int ly = by + j;
-      if (!geo.wrap && (ly < 0 || ly >= geo.lrows)) continue;
-      const int r = geo.wrap ? wrapc(ly, ny) : ly;
+      if (SLAB && (ly < 0 || ly >= geo.lrows)) continue;
+      const int r = SLAB ? ly : wrapc(ly, ny);
       const int64_t w = (int64_t)r * nx + gx;
       const int li = (ty * V + j) * 32 + tx;
 #pragma unroll
@@ -309,9 +313,17 @@ int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const TbGeo& geo, 
     kernel<<<grid, dim3(32, BY), smem, s>>>(nx, ny, geo, in, out, bits, mk, tr, tiles_x, ntiles);
     return QWB_OK;
   };
-  static bool conf_plain[256] = {}, conf_trace[256] = {};   // per instantiation and device
-  if (tr.n > 0) return go(lattice_tb_kernel<SHIFT, MARKED, T, BY, V, true>, conf_trace);
-  return go(lattice_tb_kernel<SHIFT, MARKED, T, BY, V, false>, conf_plain);
+  static bool conf_plain[256] = {}, conf_trace[256] = {}, conf_slab[256] = {};   // per instantiation, device
+  if (!geo.wrap) {
+    if constexpr (T == kSlabDepth && BY == 16 && V == 3) {
+      if (tr.n > 0) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "slab launches do not fuse traces");
+      return go(lattice_tb_kernel<SHIFT, MARKED, T, BY, V, false, true>, conf_slab);
+    } else {
+      QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "slab kernels exist for T = %d on 32x48 regions only", kSlabDepth);
+    }
+  }
+  if (tr.n > 0) return go(lattice_tb_kernel<SHIFT, MARKED, T, BY, V, true, false>, conf_trace);
+  return go(lattice_tb_kernel<SHIFT, MARKED, T, BY, V, false, false>, conf_plain);
 }
 
 template <int T, int BY, int V>
@@ -548,6 +560,10 @@ int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx
   const TbGeo geo{ny, 0, ny, 0, 1, 0};
   return tb_launch_impl(ctx, depth, shift, s, nx, ny, geo, in, out, bits, marked_host, n_marked,
                         trace_vertices_host, n_trace, trace);
+}
+
+int lattice_slab_depth(int depth) {   // the ghost-row depth a slab run can use (0: none)
+  return (lattice_kind() == 1 && depth == kSlabDepth && env_int("QWB_LATTICE_SHAPE", 3) == 3) ? depth : 0;
 }
 
 int lattice_tb_owned_rows(int depth) {

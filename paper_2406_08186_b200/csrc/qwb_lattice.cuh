@@ -236,7 +236,8 @@ struct TbGeo {
 };
 int lattice_tb_depth(int64_t nx, int64_t ny, int64_t n_marked);
 int lattice_kind();   // 1 = CTA-tile kernel, 0 = wavefront kernel
-int lattice_tb_owned_rows(int depth);   // owned rows per tile row of the tile kernel (0: n/a)
+int lattice_tb_owned_rows(int depth);
+int lattice_slab_depth(int depth);   // ghost-row depth usable by slab runs (0: none)   // owned rows per tile row of the tile kernel (0: n/a)
 int lattice_tb_launch_geo(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny, const TbGeo& geo,
                           const double2* in, double2* out, const uint32_t* bits, const int64_t* marked_host,
                           int64_t n_marked);
