@@ -380,12 +380,13 @@ def run_b200(args):
 
     extras = {}
     if not args.no_extras and not single:
-        try:
-            c4 = measure_c4_sharded(q, dev, local, rank, world, dist)
-        except Exception as e:  # pragma: no cover - reported, the headline line still prints
-            c4 = {"error": repr(e)}
-        if rank == 0:
-            extras["c4_hypercube22_sharded"] = c4
+        for name, fn in (("c5_grid8192_sharded", measure_c5_sharded), ("c4_hypercube22_sharded", measure_c4_sharded)):
+            try:
+                r = fn(q, dev, local, rank, world, dist)
+            except Exception as e:  # pragma: no cover - reported, the headline line still prints
+                r = {"error": repr(e)}
+            if rank == 0:
+                extras[name] = r
     if not args.no_extras and rank == 0:
         extras.update(measure_extras(q, CO, eng, dev, peak))
 
@@ -445,6 +446,34 @@ def run_b200(args):
     if dist:
         dist.destroy_process_group()
     return 0
+
+
+def measure_c5_sharded(q, dev, local, rank, world, dist):
+    """C5 across the ranks (strong scaling): the 8192 x 8192 torus split into
+    y-slabs (fused temporally blocked slabs + NCCL ghost rows), 100 coined
+    steps, CUDA-event time on the launch stream, max over ranks."""
+    import torch
+    from paper_2406_08186_b200 import distributed as DI
+    nx = 8192
+    eng2 = q.init_engine("b200", device=local)
+    lat = DI.SlabLattice(eng2, nx, nx, "flipflop", (), rank, world, comm=True)
+    lat.a.fill_(1.0 / (2.0 * nx))
+    stream = torch.cuda.current_stream(dev)
+    lat.advance(8)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    lat.advance(100)
+    b.record(stream)
+    torch.cuda.synchronize(dev)
+    dt = max_over_ranks(a.elapsed_time(b) / 1e3, dist, dev)
+    lat.close()
+    q.stop_engine(eng2)
+    return {"arc_updates_per_s": 4 * nx * nx * 100 / dt, "us_per_step": dt / 100 * 1e6, "ranks": world,
+            "ghost_rows": lat.ghost, "rows_per_rank": lat.rows,
+            "scaling": "strong (one 8192 x 8192 torus over all ranks)"}
 
 
 def measure_c4_sharded(q, dev, local, rank, world, dist):
@@ -511,6 +540,15 @@ def measure_extras(q, CO, eng, dev, peak):
     out["grid4096_marked"] = {"arc_updates_per_s": arcs / per, "achieved_GBps": gbs, "frac": gbs / peak,
                               "us_per_step": per * 1e6}
     del r
+    torch.cuda.empty_cache()
+    # C5 on one GPU (the efficiency denominator of the multi-GPU runs):
+    # 8192^2 torus, 8.6 GB ping-pong state, 100 coined steps
+    r5 = CO._LatticeRunner(eng, q.CoinedSpec(q.graphs.grid(8192, 8192)))
+    r5.a.fill_(1.0 / (2.0 * 8192))
+    s5 = timed(lambda: r5.advance(100), 2) / 200
+    out["c5_grid8192"] = {"arc_updates_per_s": 4 * 8192 * 8192 / s5, "us_per_step": s5 * 1e6,
+                          "state_bytes": 2 * 4 * 8192 * 8192 * 16}
+    del r5
     torch.cuda.empty_cache()
     # C3 in full: 4096^2, centre marked, uniform psi0 (= 2^-13 exactly),
     # T = ceil(sqrt(N ln N)) = 16707 steps, p(marked) after every step fused
