@@ -526,10 +526,10 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
     // Accumulators of numpy's x0 + pairwise(x1..x_m): x0, ac[0..3] take the
     // elements at row positions 1 + 4k + a, the tail (positions past
     // main_end) is added to the combined (ac0 + ac1) + (ac2 + ac3) in ac[0].
-    // A chunk's slot depends only on its index modulo 4 (set partner c at
-    // position c, clear partner c at position c + LB - 1), so the chunk loop
-    // is unrolled by 4 and every slot is a compile-time register; the own
-    // tile's ten positions start at hs, one of four compile-time rotations.
+    // A chunk's slot depends only on its index modulo 4, so the set partners,
+    // the own tile and the clear partners run as three loops unrolled by 4 in
+    // which every slot is a compile-time register (the own tile and the clear
+    // partners in one of four compile-time rotations).
     const uint32_t full_u32 = smem_u32(full), empty_u32 = smem_u32(empty);
     uint32_t s = 0, ph = 0, ti = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
@@ -569,52 +569,91 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
           }
         }
       };
-      for (int c0 = 0; c0 <= nh; c0 += 4) {
+      // one stage: wait for it, read and scale this thread's entries, release
+      auto take = [&](double2 (&e)[VPT]) {
+        mbar_wait_u32(full_u32 + 8 * s, ph);
+        const double2* ch = ring + (size_t)s * TILE;
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) e[j] = scale_real_z(g, ch[tid + j * CONS]);
+        __syncwarp();   // the scaled values are in registers: the stage may be refilled
+        if (lane == 0) mbar_arrive_u32(empty_u32 + 8 * s);
+        if (++s == NS) {
+          s = 0;
+          ph ^= 1u;
+        }
+      };
+      auto addto = [&](double2 (&acc)[VPT], const double2 (&e)[VPT]) {
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) acc[j] = cadd(acc[j], e[j]);
+      };
+      // phase A: set partners, chunk c at position c (c = 0 is x0; the slot
+      // of c >= 1 is (c - 1) & 3, so blocks of four from c = 1 are slots 0..3)
+      double2 e[VPT];
+      int c = 0;
+      if (hs > 0) {
+        take(e);
+        addto(x0, e);
+        c = 1;
+      }
+      for (; c + 4 <= hs; c += 4) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int c = c0 + u;
-          if (c <= nh) {
-            mbar_wait_u32(full_u32 + 8 * s, ph);
-            const double2* ch = ring + (size_t)s * TILE;
-            if (c == hs) {
-              switch (hs & 3) {
-                case 0: fold_own(ch, std::integral_constant<int, 0>{}); break;
-                case 1: fold_own(ch, std::integral_constant<int, 1>{}); break;
-                case 2: fold_own(ch, std::integral_constant<int, 2>{}); break;
-                default: fold_own(ch, std::integral_constant<int, 3>{}); break;
-              }
-            } else {
-              double2 e[VPT];
+          take(e);
+          addto(ac[u], e);
+        }
+      }
 #pragma unroll
-              for (int j = 0; j < VPT; ++j) e[j] = scale_real_z(g, ch[tid + j * CONS]);
-              if (c < hs) {            // set partner, position c
-                if (c == 0) {
+      for (int u = 0; u < 3; ++u)
+        if (c + u < hs) {
+          take(e);
+          addto(ac[u], e);
+        }
+      // phase B: the tile itself, positions hs .. hs + LB - 1
+      {
+        mbar_wait_u32(full_u32 + 8 * s, ph);
+        const double2* ch = ring + (size_t)s * TILE;
+        switch (hs & 3) {
+          case 0: fold_own(ch, std::integral_constant<int, 0>{}); break;
+          case 1: fold_own(ch, std::integral_constant<int, 1>{}); break;
+          case 2: fold_own(ch, std::integral_constant<int, 2>{}); break;
+          default: fold_own(ch, std::integral_constant<int, 3>{}); break;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_u32(empty_u32 + 8 * s);
+        if (++s == NS) {
+          s = 0;
+          ph ^= 1u;
+        }
+      }
+      // phase C: clear partners (partner index c from hs), position c + LB,
+      // slot (c + LB - 1) & 3; positions past main_end go to the tail
+      const int cme = max(hs, min(nh, main_end - LB + 1));
+      auto phase_c = [&](auto Rc) {
+        constexpr int R = decltype(Rc)::value;   // slot of partner hs
+        int cc = hs;
+        for (; cc + 4 <= cme; cc += 4) {
 #pragma unroll
-                  for (int j = 0; j < VPT; ++j) x0[j] = cadd(x0[j], e[j]);
-                } else {
-                  const int a = (u + 3) & 3;
-#pragma unroll
-                  for (int j = 0; j < VPT; ++j) ac[a][j] = cadd(ac[a][j], e[j]);
-                }
-              } else {                 // clear partner, position c + LB - 1
-                const int i = c + LB - 2;
-                if (i < main_end) {
-                  const int a = (u + LB - 2) & 3;
-#pragma unroll
-                  for (int j = 0; j < VPT; ++j) ac[a][j] = cadd(ac[a][j], e[j]);
-                } else {
-                  add_tail(i, e);
-                }
-              }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive_u32(empty_u32 + 8 * s);
-            if (++s == NS) {
-              s = 0;
-              ph ^= 1u;
-            }
+          for (int u = 0; u < 4; ++u) {
+            take(e);
+            addto(ac[(R + u) & 3], e);
           }
         }
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+          if (cc + u < cme) {
+            take(e);
+            addto(ac[(R + u) & 3], e);
+          }
+      };
+      switch ((hs + LB - 1) & 3) {
+        case 0: phase_c(std::integral_constant<int, 0>{}); break;
+        case 1: phase_c(std::integral_constant<int, 1>{}); break;
+        case 2: phase_c(std::integral_constant<int, 2>{}); break;
+        default: phase_c(std::integral_constant<int, 3>{}); break;
+      }
+      for (int cc = cme; cc < nh; ++cc) {
+        take(e);
+        add_tail(cc + LB - 1, e);
       }
       uint32_t mword[VPT];
 #pragma unroll
