@@ -26,6 +26,7 @@ from .backend import (
     CsrMatrix,
     DeviceCsr,
     Engine,
+    SnapshotPipe,
     builder_engine,
     csr_from_triplets,
     device_norm,
@@ -305,12 +306,17 @@ def simulate(engine: Engine, spec: CoinedSpec, sim_range, psi0: WalkState) -> li
     runner.load(x)
     states: list[WalkState] = []
     if isinstance(runner, _LatticeRunner):
+        pipe = SnapshotPipe(engine, x.numel(), len(ks))
         cur = 0
         for k in ks:
             runner.advance(k - cur)
             cur = k
-            runner.store(x)
-            arr, owner = to_host(x, pinned=True)
+            if len(ks) == 1:
+                runner.store(x)
+                pipe.capture(None, src=x)
+            else:
+                pipe.capture(runner.store)
+        for arr, owner in pipe.results():
             states.append(WalkState._adopt(basis, arr, owner))
         return states
     n = runner.n

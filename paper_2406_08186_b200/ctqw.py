@@ -21,6 +21,7 @@ from .backend import (
     CsrMatrix,
     DeviceCsr,
     Engine,
+    SnapshotPipe,
     builder_engine,
     device_norm,
     empty_z,
@@ -210,17 +211,23 @@ def simulate(engine: Engine, spec: CtqwSpec, sim_range, psi0: WalkState,
     if not (tol > 0):
         raise ValueError("tol must be positive")
     op = _Operator(engine, spec)
-    states: list[WalkState] = []
-    current = psi0
+    ks = list(rng.indices())
+    moves = sum(1 for a, b in zip([0] + ks, ks) if b != a)
+    # snapshot downloads overlap the evolution towards the next snapshot
+    pipe = SnapshotPipe(engine, x.numel(), moves)
+    which = []         # per index in the range: capture number, or -1 for psi0 itself
+    captured = 0
     cur_k = 0
-    for k in rng.indices():
+    for k in ks:
         if k != cur_k:
             op.evolve(x, (k - cur_k) * spec.delta_t, tol)
             cur_k = k
-            arr, owner = to_host(x, pinned=True)
-            current = WalkState._adopt(psi0.basis, arr, owner)
-        states.append(current)
-    return states
+            pipe.capture(lambda buf: buf.copy_(x), src=x if moves == 1 else None)
+            captured += 1
+        which.append(captured - 1)
+    res = pipe.results()
+    snaps = [WalkState._adopt(psi0.basis, arr, owner) for arr, owner in res]
+    return [psi0 if w < 0 else snaps[w] for w in which]
 
 
 def probability_distribution(states) -> list[np.ndarray]:

@@ -42,3 +42,5 @@ t("H2D torch pageable", lambda: x.copy_(hpage))
 t("D2H torch pinned tensor", lambda: hp.copy_(x))
 t("D2H torch pageable", lambda: hpage.copy_(x))
 t("pinned alloc 268MB", lambda: torch.empty(g.num_arcs, dtype=torch.complex128, pin_memory=True))
+t("simulate (0,1001,100) 11 snaps", lambda: CO.simulate(eng, spec, (0, 1001, 100), psi0), reps=2)
+t("simulate (0,10001,1000) 11 snaps", lambda: CO.simulate(eng, spec, (0, 10001, 1000), psi0), reps=1)
