@@ -58,6 +58,13 @@ __device__ __forceinline__ double2 row_value(const G& g, int64_t len) {
   return qwb::reduceat_z(g, len);
 }
 
+// two consecutive complex128 (32 B, 32-B aligned) in one 256-bit load
+__device__ __forceinline__ void ld2z(const double2* p, double2& a, double2& b) {
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
+      : "l"(p));
+}
+
 __global__ void __launch_bounds__(256)
 spmv_kernel(int64_t n_rows, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
             const double2* __restrict__ val, const double2* __restrict__ x,
@@ -65,6 +72,28 @@ spmv_kernel(int64_t n_rows, const int64_t* __restrict__ rowptr, const int32_t* _
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = __ldg(rowptr + r), e = __ldg(rowptr + r + 1);
+    if (e - s == 4 && (s & 3) == 0) {
+      // 4-entry row (every Grover row of a degree-4 head): one 128-bit column
+      // load, two 256-bit value loads; the columns are the head's arc span, so
+      // x usually comes in two 256-bit loads as well
+      const int4 c = __ldg(reinterpret_cast<const int4*>(col + s));
+      double2 v0, v1, v2, v3, x0, x1, x2, x3;
+      ld2z(val + s, v0, v1);
+      ld2z(val + s + 2, v2, v3);
+      if (c.w == c.x + 3 && c.y == c.x + 1 && c.z == c.x + 2 && (c.x & 1) == 0) {
+        ld2z(x + c.x, x0, x1);
+        ld2z(x + c.x + 2, x2, x3);
+      } else {
+        x0 = __ldg(x + c.x);
+        x1 = __ldg(x + c.y);
+        x2 = __ldg(x + c.z);
+        x3 = __ldg(x + c.w);
+      }
+      // x0 + ((x1 + x2) + x3), numpy's reduceat of a 4-entry row
+      const double2 r1 = cadd(cadd(make_double2(-0.0, -0.0), cmul_np(v1, x1)), cmul_np(v2, x2));
+      y[r] = cadd(cmul_np(v0, x0), cadd(r1, cmul_np(v3, x3)));
+      continue;
+    }
     RowGet g{col, val, x, s};
     y[r] = row_value(g, e - s);
   }
