@@ -569,6 +569,13 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
           }
         }
       };
+      // the marked-bitmap words are loaded now and land while the stream is folded
+      uint32_t mword[VPT];
+#pragma unroll
+      for (int j = 0; j < VPT; ++j) {
+        const int64_t v = ((int64_t)H << LB) + tid + j * CONS;   // global id
+        mword[j] = op.bits ? __ldg(op.bits + (v >> 5)) : 0u;
+      }
       // one stage: wait for it, read and scale this thread's entries, release
       auto take = [&](double2 (&e)[VPT]) {
         mbar_wait_u32(full_u32 + 8 * s, ph);
@@ -654,12 +661,6 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
       for (int cc = cme; cc < nh; ++cc) {
         take(e);
         add_tail(cc + LB - 1, e);
-      }
-      uint32_t mword[VPT];
-#pragma unroll
-      for (int j = 0; j < VPT; ++j) {
-        const int64_t v = ((int64_t)H << LB) + tid + j * CONS;   // global id
-        mword[j] = op.bits ? __ldg(op.bits + (v >> 5)) : 0u;
       }
       const int ab = ti & 1;
       mbar_wait(afull + ab, (ti >> 1) & 1);
