@@ -21,6 +21,8 @@
 //     the inner (32 - 2T) x (BY*V - 2T) vertices are exact and are written.
 //
 // Regions wrap around the torus (modular global coordinates): any nx, ny >= 3.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <string.h>
 
 #include "qwb_lattice.cuh"
@@ -35,6 +37,28 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+__device__ __forceinline__ void tb_mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void tb_mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tb_mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "TB_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra TB_WAIT_%=;\n"
+      "}\n" ::"r"((unsigned)__cvta_generic_to_shared(b)),
+      "r"(parity)
+      : "memory");
+}
 
 __device__ __forceinline__ int wrapc(int v, int n) {
   v = v < 0 ? v + n : v;
@@ -58,9 +82,9 @@ struct TbShape {
   static constexpr int REG = RX * RY;      // region vertices
   // stages of the next tiles' amplitudes: two (loads of two tiles in flight)
   // when they fit next to the exchange buffers, else one
-  static constexpr int NSTAGE = ((8 * (size_t)REG + 4 * (size_t)NT) * sizeof(double2) <= 232448) ? 2 : 1;
-  static constexpr size_t smem_bytes() {
-    return (4 * (size_t)REG * NSTAGE + 4 * (size_t)NT) * sizeof(double2);
+  static constexpr int NSTAGE = ((8 * (size_t)REG + 4 * (size_t)NT) * sizeof(double2) + 16 <= 232448) ? 2 : 1;
+  static constexpr size_t smem_bytes() {   // + two mbarriers for the TMA loads
+    return (4 * (size_t)REG * NSTAGE + 4 * (size_t)NT) * sizeof(double2) + 2 * sizeof(uint64_t);
   }
 };
 
@@ -167,16 +191,45 @@ template <int SHIFT, bool MARKED, int T, int BY, int V, bool TRACE, bool SLAB>
 __global__ void __launch_bounds__(32 * BY, 1)
 lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, double2* __restrict__ out,
                   const uint32_t* __restrict__ bits, MarkedList mk, TraceList tr, int tiles_x,
-                  int ntiles) {
+                  int ntiles, const __grid_constant__ CUtensorMap imap, int use_tma) {
   using S = TbShape<BY, V>;
   constexpr int OX = S::RX - 2 * T, OY = S::RY - 2 * T;   // exact (owned) block
   extern __shared__ double2 sm[];
   double2* stage0 = sm;                // [NSTAGE][4][RY][RX] next tiles' amplitudes
   double2* xD = sm + 4 * S::REG * S::NSTAGE;   // [2][BY][32] O_D of each thread's lowest row
   double2* xU = xD + 2 * S::NT;        // [2][BY][32] O_U of each thread's highest row
+  uint64_t* tbar = reinterpret_cast<uint64_t*>(xU + 2 * S::NT);   // [2] TMA-load barriers
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * 32 + tx;
   if (!SLAB) geo = TbGeo{ny, 0, ny, 0, 1, 0};   // compile-time constants for the torus
+  // Tiles whose region lies inside the torus (no wrap) load all four planes
+  // with ONE tensor TMA (box [4][RY][32] complex128) completing on a stage
+  // mbarrier; regions that wrap use per-thread cp.async.
+  const bool tma = !SLAB && use_tma;
+  if (tma) {
+    if (tid == 0) {
+      tb_mbar_init(tbar, 1);
+      tb_mbar_init(tbar + 1, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+  }
+  auto tma_ok = [&](int tcol, int trow) {
+    const int bx = tcol * OX - T, by = trow * OY - T;
+    return tma && bx >= 0 && bx + S::RX <= nx && by >= 0 && by + S::RY <= ny;
+  };
+  auto tma_load = [&](double2* stage, uint64_t* bar, int tcol, int trow) {
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // earlier LDS of this stage
+      tb_mbar_expect_tx(bar, 4u * S::REG * (uint32_t)sizeof(double2));
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+          "[%5];\n" ::"r"((unsigned)__cvta_generic_to_shared(stage)),
+          "l"(reinterpret_cast<uint64_t>(&imap)), "r"(2 * (tcol * OX - T)), "r"(trow * OY - T), "r"(0),
+          "r"((unsigned)__cvta_generic_to_shared(bar))
+          : "memory");
+    }
+  };
   const int64_t n = (int64_t)nx * geo.lrows;   // plane stride of the buffers
 
   // tile coordinates advance by gridDim.x tiles per iteration: (gdiv, gmod)
@@ -212,14 +265,26 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
   int tcol = tile % tiles_x, trow = tile / tiles_x;
   // (pcol, prow): the tile the next prefetch loads, NSTAGE - 1 tiles ahead of (tcol, trow)
   int pcol = tcol, prow = trow, ptile = tile;
+  // per stage: whether its pending load is a TMA (f) and that barrier's parity (ph)
+  bool f0 = false, f1 = false;
+  uint32_t ph0 = 0, ph1 = 0;
   for (int k = 0; k < S::NSTAGE; ++k) {
-    if (ptile < ntiles) prefetch(stage0 + (size_t)k * 4 * S::REG, pcol, prow);
+    if (ptile < ntiles) {
+      double2* st = stage0 + (size_t)k * 4 * S::REG;
+      if (tma_ok(pcol, prow)) {
+        tma_load(st, tbar + k, pcol, prow);
+        (k ? f1 : f0) = true;
+      } else {
+        prefetch(st, pcol, prow);
+      }
+    }
     cp_commit();
     advance(pcol, prow);
     ptile += gridDim.x;
   }
   for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
-    double2* stage = stage0 + (size_t)(S::NSTAGE == 2 ? (it & 1) : 0) * 4 * S::REG;
+    const int k = S::NSTAGE == 2 ? (it & 1) : 0;
+    double2* stage = stage0 + (size_t)k * 4 * S::REG;
     // x0: global column of the tile's first owned column; y0: unwrapped
     // global row of its first owned row; lyb: its local buffer row
     const int x0 = tcol * OX, y0 = geo.ybase + trow * OY, lyb = geo.own0 + trow * OY;
@@ -232,6 +297,10 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
       asm volatile("cp.async.wait_group 1;\n" ::: "memory");   // this tile's group; the next may fly
     else
       cp_wait_all();
+    if (k ? f1 : f0) {   // this stage came by TMA: wait for its bytes
+      tb_mbar_wait(tbar + k, k ? ph1 : ph0);
+      if (k) ph1 ^= 1u; else ph0 ^= 1u;
+    }
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < V; ++j) {
@@ -243,7 +312,15 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
       vU[j] = stage[3 * S::REG + li];
     }
     __syncthreads();
-    if (ptile < ntiles) prefetch(stage, pcol, prow);   // into the stage just consumed
+    if (k) f1 = false; else f0 = false;
+    if (ptile < ntiles) {   // into the stage just consumed
+      if (tma_ok(pcol, prow)) {
+        tma_load(stage, tbar + k, pcol, prow);
+        if (k) f1 = true; else f0 = true;
+      } else {
+        prefetch(stage, pcol, prow);
+      }
+    }
     cp_commit();
     advance(pcol, prow);
     ptile += gridDim.x;
@@ -293,6 +370,8 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
   cp_wait_all();
 }
 
+int env_int(const char* name, int dflt);
+
 template <int SHIFT, bool MARKED, int T, int BY, int V>
 int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const TbGeo& geo, const double2* in,
                 double2* out, const uint32_t* bits, const MarkedList& mk, const TraceList& tr) {
@@ -303,6 +382,29 @@ int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const TbGeo& geo, 
   const size_t smem = Sh::smem_bytes();
   const int cap = ctx->num_sms - geo.spare_sms > 1 ? ctx->num_sms - geo.spare_sms : 1;
   const int grid = ntiles < cap ? ntiles : cap;
+  // tensor map of the input planes for the TMA tile loads (torus launches):
+  // doubles [4][ny][2 nx], box [4][RY][64] = one stage
+  CUtensorMap imap{};
+  static int use_tma_env = env_int("QWB_LATTICE_TMA", 1);
+  int use_tma = 0;
+  if (geo.wrap && use_tma_env) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q;
+      void* fn = nullptr;
+      cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+      if (e == cudaSuccess && fn) encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    if (encode) {
+      const cuuint64_t dims[3] = {2 * (cuuint64_t)nx, (cuuint64_t)ny, 4};
+      const cuuint64_t strides[2] = {2 * (cuuint64_t)nx * sizeof(double), (cuuint64_t)nx * ny * sizeof(double2)};
+      const cuuint32_t box[3] = {2 * (cuuint32_t)Sh::RX, (cuuint32_t)Sh::RY, 4};
+      const cuuint32_t estr[3] = {1, 1, 1};
+      use_tma = encode(&imap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double2*>(in), dims, strides, box,
+                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+  }
   auto go = [&](auto kernel, bool* configured) -> int {
     const int dev = ctx->device & 255;
     if (!configured[dev]) {
@@ -310,7 +412,7 @@ int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const TbGeo& geo, 
       if (e != cudaSuccess) return qwb::cuda_status(ctx, e, "cudaFuncSetAttribute(lattice_tb)");
       configured[dev] = true;
     }
-    kernel<<<grid, dim3(32, BY), smem, s>>>(nx, ny, geo, in, out, bits, mk, tr, tiles_x, ntiles);
+    kernel<<<grid, dim3(32, BY), smem, s>>>(nx, ny, geo, in, out, bits, mk, tr, tiles_x, ntiles, imap, use_tma);
     return QWB_OK;
   };
   static bool conf_plain[256] = {}, conf_trace[256] = {}, conf_slab[256] = {};   // per instantiation, device
