@@ -205,7 +205,7 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
   // Tiles whose region lies inside the torus (no wrap) load all four planes
   // with ONE tensor TMA (box [4][RY][32] complex128) completing on a stage
   // mbarrier; regions that wrap use per-thread cp.async.
-  const bool tma = !SLAB && use_tma;
+  const bool tma = use_tma;
   if (tma) {
     if (tid == 0) {
       tb_mbar_init(tbar, 1);
@@ -214,9 +214,9 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
     }
     __syncthreads();
   }
-  auto tma_ok = [&](int tcol, int trow) {
-    const int bx = tcol * OX - T, by = trow * OY - T;
-    return tma && bx >= 0 && bx + S::RX <= nx && by >= 0 && by + S::RY <= ny;
+  auto tma_ok = [&](int tcol, int trow) {   // the region lies inside the buffer (no wrap)
+    const int bx = tcol * OX - T, by = geo.own0 + trow * OY - T;
+    return tma && bx >= 0 && bx + S::RX <= nx && by >= 0 && by + S::RY <= geo.lrows;
   };
   auto tma_load = [&](double2* stage, uint64_t* bar, int tcol, int trow) {
     if (tid == 0) {
@@ -225,7 +225,7 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
       asm volatile(
           "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
           "[%5];\n" ::"r"((unsigned)__cvta_generic_to_shared(stage)),
-          "l"(reinterpret_cast<uint64_t>(&imap)), "r"(2 * (tcol * OX - T)), "r"(trow * OY - T), "r"(0),
+          "l"(reinterpret_cast<uint64_t>(&imap)), "r"(2 * (tcol * OX - T)), "r"(geo.own0 + trow * OY - T), "r"(0),
           "r"((unsigned)__cvta_generic_to_shared(bar))
           : "memory");
     }
@@ -382,12 +382,13 @@ int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const TbGeo& geo, 
   const size_t smem = Sh::smem_bytes();
   const int cap = ctx->num_sms - geo.spare_sms > 1 ? ctx->num_sms - geo.spare_sms : 1;
   const int grid = ntiles < cap ? ntiles : cap;
-  // tensor map of the input planes for the TMA tile loads (torus launches):
-  // doubles [4][ny][2 nx], box [4][RY][64] = one stage
+  // tensor map of the input planes for the TMA tile loads: doubles
+  // [4][lrows][2 nx] (lrows = ny on the torus, the slab's buffer rows), box
+  // [4][RY][64] = one stage
   CUtensorMap imap{};
   static int use_tma_env = env_int("QWB_LATTICE_TMA", 1);
   int use_tma = 0;
-  if (geo.wrap && use_tma_env) {
+  if (use_tma_env) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
       cudaDriverEntryPointQueryResult q;
@@ -396,8 +397,9 @@ int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const TbGeo& geo, 
       if (e == cudaSuccess && fn) encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
     if (encode) {
-      const cuuint64_t dims[3] = {2 * (cuuint64_t)nx, (cuuint64_t)ny, 4};
-      const cuuint64_t strides[2] = {2 * (cuuint64_t)nx * sizeof(double), (cuuint64_t)nx * ny * sizeof(double2)};
+      const cuuint64_t dims[3] = {2 * (cuuint64_t)nx, (cuuint64_t)geo.lrows, 4};
+      const cuuint64_t strides[2] = {2 * (cuuint64_t)nx * sizeof(double),
+                                     (cuuint64_t)nx * geo.lrows * sizeof(double2)};
       const cuuint32_t box[3] = {2 * (cuuint32_t)Sh::RX, (cuuint32_t)Sh::RY, 4};
       const cuuint32_t estr[3] = {1, 1, 1};
       use_tma = encode(&imap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double2*>(in), dims, strides, box,
