@@ -322,7 +322,7 @@ def run_b200(args):
         depth = dep.value
         if depth > 0:
             per_walk = walk // depth + walk % depth
-            kernel = (f"lattice_tb_kernel<flipflop, T={depth}, 32x48 region>" if knd.value == 1
+            kernel = (f"lattice_tb_kernel<flipflop, T={depth}, 32x64 region>" if knd.value == 1
                       else f"lattice_wf_kernel<flipflop, T={depth}>")
         else:
             per_walk = walk
@@ -332,7 +332,7 @@ def run_b200(args):
         # exchange, then the two edge bands; remainder steps one at a time
         depth = runner.ghost
         per_walk = 3 * (walk // depth) + walk % depth
-        kernel = f"lattice_tb_kernel<flipflop, T={depth}, 32x48 region> on y-slabs with {depth} ghost rows"
+        kernel = f"lattice_tb_kernel<flipflop, T={depth}, 32x64 region> on y-slabs with {depth} ghost rows"
     else:
         depth = 0
         per_walk = 2 * walk

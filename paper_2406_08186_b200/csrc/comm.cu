@@ -277,6 +277,12 @@ int qwb_csr_halo_exchange(qwb_ctx* ctx, int64_t n_local, qwb_z* x_ext, const int
 // plane's first g owned rows go to the rank below's top ghost rows, the last
 // g owned rows to the rank above's bottom ghost rows (g = ghost before a
 // temporally blocked launch, 1 before a single pull step).
+// the ghost rows of launch `v` have landed: everything queued before this
+// kernel on the comm stream (the NCCL group) is complete
+static __global__ void raise_flag_kernel(int* flag, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(flag), "r"(v) : "memory");
+}
+
 static int ghost_exchange_nccl(qwb_ctx* ctx, int64_t nx, int64_t nl, int64_t G, int g, double2* planes,
                                int below, int above, cudaStream_t s) {
   NcclComm comm = (NcclComm)ctx->comm;
@@ -320,7 +326,13 @@ int qwb_slab_run_fused(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t
     const char* e = getenv("QWB_SLAB_SPLIT");
     split_env = (e && *e) ? atoi(e) : 1;
   }
-  const bool split = split_env && band > 0 && ny_local >= 3 * (int64_t)band;
+  const int ntr = band > 0 ? (int)((ny_local + band - 1) / band) : 0;   // tile rows of the slab
+  const bool split = split_env && ntr >= 3;
+  if (split && !ctx->ghost_flag) {
+    QWB_CUDA(ctx, cudaMalloc(&ctx->ghost_flag, sizeof(int)));
+    QWB_CUDA(ctx, cudaMemsetAsync(ctx->ghost_flag, 0, sizeof(int), s));
+    ctx->ghost_seq = 0;
+  }
   int swaps = 0;
   for (int64_t k = 0; k < steps;) {
     const int g = (k + ghost <= steps) ? (int)ghost : 1;
@@ -330,21 +342,19 @@ int qwb_slab_run_fused(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t
       QWB_CUDA(ctx, cudaStreamWaitEvent(cs, ctx->ev_ready, 0));
       st = ghost_exchange_nccl(ctx, nx, ny_local, ghost, g, cur, rank_below, rank_above, cs);
       if (st) return st;
+      raise_flag_kernel<<<1, 1, 0, cs>>>(ctx->ghost_flag, ctx->ghost_seq + 1);
+      QWB_LAUNCH_CHECK(ctx, "raise_flag_kernel");
       QWB_CUDA(ctx, cudaEventRecord(ctx->ev_done, cs));
       const int lr = (int)(ny_local + 2 * ghost);
-      const qwb::TbGeo mid{lr, (int)ghost + band, (int)ny_local - 2 * band, (int)y0 + band, 0, 4};
-      st = qwb::lattice_tb_launch_geo(ctx, g, shift, s, (int)nx, (int)ny, mid, cur, nxt, marked_bits, marked_host,
+      // ONE launch: the middle tile rows first (they read no ghost row) while
+      // the exchange runs on the comm stream, then the two edge rows, whose
+      // CTAs wait for the device flag raised after the exchange
+      const int seq = ++ctx->ghost_seq;
+      const qwb::TbGeo geo{lr, (int)ghost, (int)ny_local, (int)y0, 0, 4, ntr, ctx->ghost_flag, seq};
+      st = qwb::lattice_tb_launch_geo(ctx, g, shift, s, (int)nx, (int)ny, geo, cur, nxt, marked_bits, marked_host,
                                       n_marked);
       if (st) return st;
-      QWB_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_done, 0));
-      const qwb::TbGeo lo{lr, (int)ghost, band, (int)y0, 0, 0};
-      const qwb::TbGeo hi{lr, (int)(ghost + ny_local) - band, band, (int)(y0 + ny_local) - band, 0, 0};
-      st = qwb::lattice_tb_launch_geo(ctx, g, shift, s, (int)nx, (int)ny, lo, cur, nxt, marked_bits, marked_host,
-                                      n_marked);
-      if (!st)
-        st = qwb::lattice_tb_launch_geo(ctx, g, shift, s, (int)nx, (int)ny, hi, cur, nxt, marked_bits,
-                                        marked_host, n_marked);
-      if (st) return st;
+      QWB_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_done, 0));   // the comm stream's work precedes the next step
       QWB_LAUNCH_CHECK(ctx, "lattice_tb_kernel(slab bands)");
     } else {
       st = ghost_exchange_nccl(ctx, nx, ny_local, ghost, g, cur, rank_below, rank_above, s);

@@ -201,7 +201,7 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
   uint64_t* tbar = reinterpret_cast<uint64_t*>(xU + 2 * S::NT);   // [2] TMA-load barriers
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * 32 + tx;
-  if (!SLAB) geo = TbGeo{ny, 0, ny, 0, 1, 0};   // compile-time constants for the torus
+  if (!SLAB) geo = TbGeo{ny, 0, ny, 0, 1, 0, 0, nullptr, 0};   // compile-time constants for the torus
   // Tiles whose region lies inside the torus (no wrap) load all four planes
   // with ONE tensor TMA (box [4][RY][32] complex128) completing on a stage
   // mbarrier; regions that wrap use per-thread cp.async.
@@ -243,6 +243,26 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
       ++r;
     }
   };
+  // mid-first slab launches: virtual tile row r < ntr - 2 is row r + 1, then
+  // the edge rows 0 and ntr - 1 (which wait for the ghost rows)
+  const bool midfirst = SLAB && geo.ntr >= 3;
+  auto rmap = [&](int r) {
+    if (!midfirst) return r;
+    return r < geo.ntr - 2 ? r + 1 : (r == geo.ntr - 2 ? 0 : geo.ntr - 1);
+  };
+  bool ghosts_ready = !midfirst || geo.ready == nullptr;
+  auto need_ghosts = [&](int vr) {   // CTA-uniform call sites only
+    if (ghosts_ready || vr < geo.ntr - 2) return;
+    if (tid == 0) {
+      int v;
+      do {
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(geo.ready) : "memory");
+      } while (v < geo.ready_val);
+      asm volatile("fence.proxy.async.global;\n" ::: "memory");   // TMA reads after the acquire
+    }
+    __syncthreads();
+    ghosts_ready = true;
+  };
   auto prefetch = [&](double2* stage, int tcol, int trow) {
     const int bx = tcol * OX - T + tx;
     const int by = geo.own0 + trow * OY - T + ty * V;   // local buffer row
@@ -271,11 +291,12 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
   for (int k = 0; k < S::NSTAGE; ++k) {
     if (ptile < ntiles) {
       double2* st = stage0 + (size_t)k * 4 * S::REG;
-      if (tma_ok(pcol, prow)) {
-        tma_load(st, tbar + k, pcol, prow);
+      need_ghosts(prow);
+      if (tma_ok(pcol, rmap(prow))) {
+        tma_load(st, tbar + k, pcol, rmap(prow));
         (k ? f1 : f0) = true;
       } else {
-        prefetch(st, pcol, prow);
+        prefetch(st, pcol, rmap(prow));
       }
     }
     cp_commit();
@@ -287,8 +308,8 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
     double2* stage = stage0 + (size_t)k * 4 * S::REG;
     // x0: global column of the tile's first owned column; y0: unwrapped
     // global row of its first owned row; lyb: its local buffer row
-    const int x0 = tcol * OX, y0 = geo.ybase + trow * OY, lyb = geo.own0 + trow * OY;
-    const int trow_now = trow;
+    const int trow_now = rmap(trow);
+    const int x0 = tcol * OX, y0 = geo.ybase + trow_now * OY, lyb = geo.own0 + trow_now * OY;
     advance(tcol, trow);
     const int gx = wrapc(x0 - T + tx, nx);
     int gy[V];
@@ -314,11 +335,12 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
     __syncthreads();
     if (k) f1 = false; else f0 = false;
     if (ptile < ntiles) {   // into the stage just consumed
-      if (tma_ok(pcol, prow)) {
-        tma_load(stage, tbar + k, pcol, prow);
+      need_ghosts(prow);
+      if (tma_ok(pcol, rmap(prow))) {
+        tma_load(stage, tbar + k, pcol, rmap(prow));
         if (k) f1 = true; else f0 = true;
       } else {
-        prefetch(stage, pcol, prow);
+        prefetch(stage, pcol, rmap(prow));
       }
     }
     cp_commit();
@@ -377,7 +399,7 @@ int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const TbGeo& geo, 
                 double2* out, const uint32_t* bits, const MarkedList& mk, const TraceList& tr) {
   using Sh = TbShape<BY, V>;
   constexpr int OX = Sh::RX - 2 * T, OY = Sh::RY - 2 * T;
-  const int tiles_x = (nx + OX - 1) / OX, tiles_y = (geo.nown + OY - 1) / OY;
+  const int tiles_x = (nx + OX - 1) / OX, tiles_y = geo.ntr >= 3 ? geo.ntr : (geo.nown + OY - 1) / OY;
   const int ntiles = tiles_x * tiles_y;
   const size_t smem = Sh::smem_bytes();
   const int cap = ctx->num_sms - geo.spare_sms > 1 ? ctx->num_sms - geo.spare_sms : 1;
@@ -419,11 +441,11 @@ int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const TbGeo& geo, 
   };
   static bool conf_plain[256] = {}, conf_trace[256] = {}, conf_slab[256] = {};   // per instantiation, device
   if (!geo.wrap) {
-    if constexpr (T == kSlabDepth && BY == 16 && V == 3) {
+    if constexpr (T == kSlabDepth && BY == 16 && V == 4) {
       if (tr.n > 0) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "slab launches do not fuse traces");
       return go(lattice_tb_kernel<SHIFT, MARKED, T, BY, V, false, true>, conf_slab);
     } else {
-      QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "slab kernels exist for T = %d on 32x48 regions only", kSlabDepth);
+      QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "slab kernels exist for T = %d on 32x64 regions only", kSlabDepth);
     }
   }
   if (tr.n > 0) return go(lattice_tb_kernel<SHIFT, MARKED, T, BY, V, true, false>, conf_trace);
@@ -621,7 +643,7 @@ static int tb_launch_impl(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, in
     }
   }
   static int shape = -1;
-  if (shape < 0) shape = env_int("QWB_LATTICE_SHAPE", 3);
+  if (shape < 0) shape = env_int("QWB_LATTICE_SHAPE", 4);
   if (depth > 6) depth = 6;
   MarkedList mk{};
   mk.n = n_marked <= 8 ? (int)n_marked : -1;
@@ -639,11 +661,13 @@ static int tb_launch_impl(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, in
     tl.y[k] = (int)(trace_vertices_host[k] / nx);
   }
   // shape 1: 32x16 threads, 2 rows each (32x32 region); 2: 32x24 threads, 2 rows
-  // each (32x48 region); 3: 32x16 threads, 3 rows each (32x48 region)
+  // each (32x48 region); 3: 32x16 threads, 3 rows each (32x48 region); 4 (default):
+  // 32x16 threads, 4 rows each (32x64 region)
 #define QWB_TB_CASE(T_)                                                                        \
   case T_:                                                                                     \
     if (shape == 2) return launch_tb<T_, 24, 2>(ctx, shift, s, nx, ny, geo, in, out, bits, mk, tl); \
     if (shape == 3) return launch_tb<T_, 16, 3>(ctx, shift, s, nx, ny, geo, in, out, bits, mk, tl); \
+    if (shape == 4) return launch_tb<T_, 16, 4>(ctx, shift, s, nx, ny, geo, in, out, bits, mk, tl); \
     return launch_tb<T_, 16, 2>(ctx, shift, s, nx, ny, geo, in, out, bits, mk, tl);
   switch (depth) {
     QWB_TB_CASE(2)
@@ -661,19 +685,19 @@ int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx
                       const double2* in, double2* out, const uint32_t* bits,
                       const int64_t* marked_host, int64_t n_marked,
                       const int64_t* trace_vertices_host, int n_trace, double* trace) {
-  const TbGeo geo{ny, 0, ny, 0, 1, 0};
+  const TbGeo geo{ny, 0, ny, 0, 1, 0, 0, nullptr, 0};
   return tb_launch_impl(ctx, depth, shift, s, nx, ny, geo, in, out, bits, marked_host, n_marked,
                         trace_vertices_host, n_trace, trace);
 }
 
 int lattice_slab_depth(int depth) {   // the ghost-row depth a slab run can use (0: none)
-  return (lattice_kind() == 1 && depth == kSlabDepth && env_int("QWB_LATTICE_SHAPE", 3) == 3) ? depth : 0;
+  return (lattice_kind() == 1 && depth == kSlabDepth && env_int("QWB_LATTICE_SHAPE", 4) == 4) ? depth : 0;
 }
 
 int lattice_tb_owned_rows(int depth) {
   if (lattice_kind() != 1 || depth < 2) return 0;
-  const int shape = env_int("QWB_LATTICE_SHAPE", 3);
-  const int ry = shape == 2 ? 24 * 2 : shape == 3 ? 16 * 3 : 16 * 2;
+  const int shape = env_int("QWB_LATTICE_SHAPE", 4);
+  const int ry = shape == 2 ? 24 * 2 : shape == 3 ? 16 * 3 : shape == 4 ? 16 * 4 : 16 * 2;
   return ry - 2 * (depth > 6 ? 6 : depth);
 }
 

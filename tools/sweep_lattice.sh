@@ -1,8 +1,9 @@
-# usage: tools/sweep_lattice.sh "shape T" ...   (kernel variant sweep, 2048^2 flip-flop)
+# usage: tools/sweep_lattice.sh "shape T" ...   (kernel variant sweep: device time per coined step)
 for cfg in "$@"; do
   set -- $cfg
   if [ "$1" = "wf" ]; then export QWB_LATTICE_KIND=wf; unset QWB_LATTICE_SHAPE; else unset QWB_LATTICE_KIND; export QWB_LATTICE_SHAPE=$1; fi
   export QWB_LATTICE_T=$2
-  v=$(timeout 120 python bench.py --steps 5 --warmup 3 --walk-steps 240 --no-extras --no-cpu 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print(round(d['value']/1e9,1), round(d['roofline']['time_per_launch_us'],1))")
-  echo "$cfg -> $v" >> gpurun_out/sweep.log
+  for nx in 2048 4096; do
+    echo "shape $1 T $2: $(timeout 120 python tools/time_lattice.py $nx 2>&1 | tail -1)" >> gpurun_out/sweep.log
+  done
 done
