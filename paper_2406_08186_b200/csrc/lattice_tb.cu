@@ -642,8 +642,11 @@ static int tb_launch_impl(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, in
       default: QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "unsupported temporal block depth %d", depth);
     }
   }
-  static int shape = -1;
-  if (shape < 0) shape = env_int("QWB_LATTICE_SHAPE", 4);
+  static int shape_env = -1;
+  if (shape_env < 0) shape_env = env_int("QWB_LATTICE_SHAPE", 4);
+  // traced launches use the 3-rows-per-thread shape: with 4 rows the trace
+  // variant runs out of registers (136 vs 115 us/step at 4096^2)
+  const int shape = (trace && shape_env == 4) ? 3 : shape_env;
   if (depth > 6) depth = 6;
   MarkedList mk{};
   mk.n = n_marked <= 8 ? (int)n_marked : -1;
