@@ -663,15 +663,13 @@ static int tb_launch_impl(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, in
     tl.x[k] = (int)(trace_vertices_host[k] % nx);
     tl.y[k] = (int)(trace_vertices_host[k] / nx);
   }
-  // shape 1: 32x16 threads, 2 rows each (32x32 region); 2: 32x24 threads, 2 rows
-  // each (32x48 region); 3: 32x16 threads, 3 rows each (32x48 region); 4 (default):
-  // 32x16 threads, 4 rows each (32x64 region)
+  // shape 4 (default): 32x16 threads, 4 rows each (32x64 region); 3: 32x16
+  // threads, 3 rows each (32x48 region; traced launches).  The 32x32 and
+  // 24-warp 32x48 shapes measured slower and are not built.
 #define QWB_TB_CASE(T_)                                                                        \
   case T_:                                                                                     \
-    if (shape == 2) return launch_tb<T_, 24, 2>(ctx, shift, s, nx, ny, geo, in, out, bits, mk, tl); \
     if (shape == 3) return launch_tb<T_, 16, 3>(ctx, shift, s, nx, ny, geo, in, out, bits, mk, tl); \
-    if (shape == 4) return launch_tb<T_, 16, 4>(ctx, shift, s, nx, ny, geo, in, out, bits, mk, tl); \
-    return launch_tb<T_, 16, 2>(ctx, shift, s, nx, ny, geo, in, out, bits, mk, tl);
+    return launch_tb<T_, 16, 4>(ctx, shift, s, nx, ny, geo, in, out, bits, mk, tl);
   switch (depth) {
     QWB_TB_CASE(2)
     QWB_TB_CASE(3)
@@ -700,7 +698,7 @@ int lattice_slab_depth(int depth) {   // the ghost-row depth a slab run can use 
 int lattice_tb_owned_rows(int depth) {
   if (lattice_kind() != 1 || depth < 2) return 0;
   const int shape = env_int("QWB_LATTICE_SHAPE", 4);
-  const int ry = shape == 2 ? 24 * 2 : shape == 3 ? 16 * 3 : shape == 4 ? 16 * 4 : 16 * 2;
+  const int ry = shape == 3 ? 16 * 3 : 16 * 4;
   return ry - 2 * (depth > 6 ? 6 : depth);
 }
 
