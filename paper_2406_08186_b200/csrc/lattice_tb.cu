@@ -7,8 +7,11 @@
 // owns V vertically adjacent vertices with their 4 direction amplitudes in
 // registers:
 //
-//   * the region's state arrives by cp.async into shared memory, prefetched one
-//     tile ahead, so HBM reads overlap the arithmetic of the current tile;
+//   * the region's state arrives in shared memory one or two tiles ahead of its
+//     use, so HBM reads overlap the arithmetic of the current tile: regions
+//     inside the buffer with ONE tensor TMA (box [4 planes][BY*V rows][32]
+//     complex128, completion on a stage mbarrier), regions that wrap around
+//     the torus with per-thread 16-B cp.async;
 //   * T steps run on chip, in doubled space (qwb_lattice.cuh "doubled-space
 //     forms": the operator 2U needs additions only — 20 FP64 adds per vertex
 //     and step — and the state is scaled by 2^-T on the way out, so the result
@@ -21,6 +24,10 @@
 //     the inner (32 - 2T) x (BY*V - 2T) vertices are exact and are written.
 //
 // Regions wrap around the torus (modular global coordinates): any nx, ny >= 3.
+// The same kernel runs on multi-GPU y-slabs with ghost state rows (SLAB,
+// TbGeo): owned rows only, no y-wrap, optionally waiting on a device flag
+// before the tiles that read the ghost rows (comm.cu qwb_slab_run_fused).
+// Default tile: 16 warps x 4 rows (32 x 64 region), T = 4.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <string.h>
