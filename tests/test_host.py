@@ -4,7 +4,6 @@ behaves like the reference.  No kernel is launched here."""
 
 from __future__ import annotations
 
-import ctypes as C
 import os
 import re
 import subprocess
