@@ -80,6 +80,7 @@ __device__ __forceinline__ double2 shfl_up2(double2 v) {
 }
 
 constexpr int kSlabDepth = 4;   // the slab (ghost-row) kernels are built for this depth
+constexpr size_t kTraceRecBytes = 6 * 8 * 4 * sizeof(double2);   // [T <= 6][8 vertices][4 planes]
 
 template <int BY, int V>
 struct TbShape {
@@ -89,9 +90,11 @@ struct TbShape {
   static constexpr int REG = RX * RY;      // region vertices
   // stages of the next tiles' amplitudes: two (loads of two tiles in flight)
   // when they fit next to the exchange buffers, else one
-  static constexpr int NSTAGE = ((8 * (size_t)REG + 4 * (size_t)NT) * sizeof(double2) + 16 <= 232448) ? 2 : 1;
-  static constexpr size_t smem_bytes() {   // + two mbarriers for the TMA loads
-    return (4 * (size_t)REG * NSTAGE + 4 * (size_t)NT) * sizeof(double2) + 2 * sizeof(uint64_t);
+  static constexpr int NSTAGE =
+      ((8 * (size_t)REG + 4 * (size_t)NT) * sizeof(double2) + 16 + kTraceRecBytes <= 232448) ? 2 : 1;
+  static constexpr size_t smem_bytes() {   // + two mbarriers for the TMA loads + the trace record
+    return (4 * (size_t)REG * NSTAGE + 4 * (size_t)NT) * sizeof(double2) + 2 * sizeof(uint64_t) +
+           kTraceRecBytes;
   }
 };
 
@@ -104,27 +107,26 @@ struct TraceList {
   double* out;
 };
 
-// p of a traced vertex from its level-t (doubled-space) amplitudes: unscale,
-// reference slot order, numpy |z|^2 and row sum.  Out of line: only the
-// thread owning a traced vertex calls it, the hot loops keep their code size.
-__device__ __noinline__ void trace_emit(int gx, int gy, int nx, int ny, double sc, double2 vD, double2 vL,
-                                        double2 vR, double2 vU, double* out) {
-  const auto un = [&](double2 a) { return make_double2(__dmul_rn(a.x, sc), __dmul_rn(a.y, sc)); };
-  const qwb::Slots o = qwb::order_slots(gx, gy, nx, ny, un(vD), un(vL), un(vR), un(vU));
+// p of a traced vertex from its level-t (doubled-space) amplitudes a[0..3]
+// (planes D, L, R, U): unscale, reference slot order, numpy |z|^2, row sum.
+__device__ __forceinline__ double trace_p(int gx, int gy, int nx, int ny, double sc, const double2* a) {
+  const auto un = [&](double2 z) { return make_double2(__dmul_rn(z.x, sc), __dmul_rn(z.y, sc)); };
+  const qwb::Slots o = qwb::order_slots(gx, gy, nx, ny, un(a[0]), un(a[1]), un(a[2]), un(a[3]));
   const double m0 = qwb::abs2_np(o.s0), m1 = qwb::abs2_np(o.s1), m2 = qwb::abs2_np(o.s2), m3 = qwb::abs2_np(o.s3);
-  *out = __dadd_rn(m0, __dadd_rn(__dadd_rn(m1, m2), m3));
+  return __dadd_rn(m0, __dadd_rn(__dadd_rn(m1, m2), m3));
 }
 
 // T steps of a tile on chip (see the file comment).  INTERIOR: every vertex of
 // the region is an unmarked, untraced interior vertex (no slot permutation, no
-// branches).  TRACE: emit p of the state before each step for traced vertices
-// this tile owns (the exact inner block), unscaled from doubled space.
+// branches).  TRACE: record the level-t amplitudes of the traced vertices this
+// tile owns (the exact inner block) in trbuf[t][k][4]; p is computed after
+// the steps (no call and no extra registers in the step loop).
 template <int SHIFT, bool MARKED, int T, int BY, int V, bool INTERIOR, bool TRACE>
 __device__ __forceinline__ void tile_steps(int nx, int ny, int gx, const int (&gy)[V],
                                            const uint32_t* __restrict__ bits, double2 (&vD)[V],
                                            double2 (&vL)[V], double2 (&vR)[V], double2 (&vU)[V],
                                            double2* xD, double2* xU, int tid, int ty,
-                                           const TraceList& tr, const bool (&own)[V]) {
+                                           const TraceList& tr, const bool (&own)[V], double2* trbuf) {
   bool mk[V];
 #pragma unroll
   for (int j = 0; j < V; ++j) {
@@ -144,9 +146,11 @@ __device__ __forceinline__ void tile_steps(int nx, int ny, int gx, const int (&g
 #pragma unroll
         for (int k = 0; k < 8; ++k) {   // static indices: tr stays in the param space
           if (k >= tr.n || tr.v[k] != wg) continue;
-          // level t holds 2^t psi_t
-          trace_emit(gx, gy[j], nx, ny, 1.0 / (double)(1 << t), vD[j], vL[j], vR[j], vU[j],
-                     tr.out + t * tr.n + k);
+          double2* a = trbuf + (t * 8 + k) * 4;   // level t holds 2^t psi_t
+          a[0] = vD[j];
+          a[1] = vL[j];
+          a[2] = vR[j];
+          a[3] = vU[j];
         }
       }
     }
@@ -206,6 +210,7 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
   double2* xD = sm + 4 * S::REG * S::NSTAGE;   // [2][BY][32] O_D of each thread's lowest row
   double2* xU = xD + 2 * S::NT;        // [2][BY][32] O_U of each thread's highest row
   uint64_t* tbar = reinterpret_cast<uint64_t*>(xU + 2 * S::NT);   // [2] TMA-load barriers
+  double2* trbuf = reinterpret_cast<double2*>(tbar + 2);          // [T][8][4] traced amplitudes (TRACE)
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * 32 + tx;
   if (!SLAB) geo = TbGeo{ny, 0, ny, 0, 1, 0, 0, nullptr, 0};   // compile-time constants for the torus
@@ -378,12 +383,24 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
       const int ly = ty * V + j;
       own[j] = col_ok && ly >= T && ly < T + OY && trow_now * OY + ly - T < geo.nown;
     }
-    if (interior)
+    if (interior) {
       tile_steps<SHIFT, false, T, BY, V, true, false>(nx, ny, gx, gy, bits, vD, vL, vR, vU, xD, xU,
-                                                      tid, ty, tr, own);
-    else
+                                                      tid, ty, tr, own, trbuf);
+    } else {
       tile_steps<SHIFT, MARKED, T, BY, V, false, TRACE>(nx, ny, gx, gy, bits, vD, vL, vR, vU, xD, xU,
-                                                        tid, ty, tr, own);
+                                                        tid, ty, tr, own, trbuf);
+      if (TRACE) {   // p of the traced vertices this tile owns, every level
+        __syncthreads();
+        if (tid < T * 8) {
+          const int t = tid >> 3, k = tid & 7;
+          const int mx = tr.x[k < tr.n ? k : 0], my = tr.y[k < tr.n ? k : 0];
+          const bool mine = k < tr.n && mx >= x0 && mx < x0 + OX && mx < nx && my >= y0 && my < y0 + OY &&
+                            my - y0 + trow_now * OY < geo.nown;
+          if (mine)
+            tr.out[t * tr.n + k] = trace_p(mx, my, nx, ny, 1.0 / (double)(1 << t), trbuf + (t * 8 + k) * 4);
+        }
+      }
+    }
     constexpr double kScale = 1.0 / (double)(1 << T);   // undo the doubled-space steps (exact)
 #pragma unroll
     for (int j = 0; j < V; ++j) {
@@ -651,9 +668,8 @@ static int tb_launch_impl(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, in
   }
   static int shape_env = -1;
   if (shape_env < 0) shape_env = env_int("QWB_LATTICE_SHAPE", 4);
-  // traced launches use the 3-rows-per-thread shape: with 4 rows the trace
-  // variant runs out of registers (136 vs 115 us/step at 4096^2)
-  const int shape = (trace && shape_env == 4) ? 3 : shape_env;
+  static int trace_shape = env_int("QWB_LATTICE_TRACE_SHAPE", 4);
+  const int shape = trace ? trace_shape : shape_env;
   if (depth > 6) depth = 6;
   MarkedList mk{};
   mk.n = n_marked <= 8 ? (int)n_marked : -1;
