@@ -143,11 +143,11 @@ int qwb_lattice_from_planes(qwb_ctx* ctx, int64_t nx, int64_t ny, const qwb_z* p
                             void* stream);
 /* Run `steps` coined steps ping-ponging between a (input) and b.  On return
  * *final_in_b_host says where the result is.  The marked set is passed both as
- * the device bitmap and as the sorted host list (marked_host[n_marked]); with
- * <= 8 marked vertices and no trace, several steps are fused per HBM pass
- * (temporally blocked wavefront kernel, lattice_tb.cu).  If trace != NULL,
- * trace[s*n_trace+j] receives p(trace_vertices_host[j]) of the state BEFORE
- * step s (s < steps), fused into the step kernel
+ * the device bitmap and as the sorted host list (marked_host[n_marked]).  On
+ * lattices >= 64 x 64, T = 4 steps are fused per HBM pass (temporally blocked
+ * tile kernel, lattice_tb.cu; remainder steps one at a time).  If trace !=
+ * NULL, trace[s*n_trace+j] (n_trace <= 8) receives p(trace_vertices_host[j])
+ * of the state BEFORE step s (s < steps), fused into the step kernels
  * (coined.probability_distribution semantics).                               */
 int qwb_lattice_run(qwb_ctx* ctx, int64_t nx, int64_t ny, int shift, const uint32_t* marked_bits,
                     const int64_t* marked_host, int64_t n_marked, qwb_z* a, qwb_z* b, int64_t steps,
