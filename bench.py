@@ -410,7 +410,7 @@ def run_b200(args):
                             (f"grid {nx}x{nx * world} torus split in {world} y-slabs of {nx}x{nx} "
                              f"({arcs} arcs per GPU), flip-flop Grover, {walk} coined steps per bench step, "
                              f"temporally blocked slabs: NCCL exchange of {runner.ghost} ghost state rows per "
-                             f"plane and side every {runner.ghost} steps, overlapped with the middle band"),
+                             f"plane and side every {runner.ghost} steps, in stream order before each launch"),
                 "nx": nx, "ny": nx * world, "arcs": arcs * world, "coined_steps_per_bench_step": walk,
                 "psi0": "dense random complex128 (seeded per rank), normalised",
                 "l2": f"inputs larger than L2: 2 x {16 * arcs / 1e6:.0f} MB ping-pong state per GPU (> 126 MB L2)",

@@ -277,12 +277,6 @@ int qwb_csr_halo_exchange(qwb_ctx* ctx, int64_t n_local, qwb_z* x_ext, const int
 // plane's first g owned rows go to the rank below's top ghost rows, the last
 // g owned rows to the rank above's bottom ghost rows (g = ghost before a
 // temporally blocked launch, 1 before a single pull step).
-// the ghost rows of launch `v` have landed: everything queued before this
-// kernel on the comm stream (the NCCL group) is complete
-static __global__ void raise_flag_kernel(int* flag, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(flag), "r"(v) : "memory");
-}
-
 static int ghost_exchange_nccl(qwb_ctx* ctx, int64_t nx, int64_t nl, int64_t G, int g, double2* planes,
                                int below, int above, cudaStream_t s) {
   NcclComm comm = (NcclComm)ctx->comm;
@@ -313,56 +307,21 @@ int qwb_slab_run_fused(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t
     QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "neighbour ranks out of range");
   if (steps < 0) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "steps must be >= 0");
   cudaStream_t s = qwb::as_stream(stream);
-  cudaStream_t cs = ctx->comm_stream;
   double2* cur = reinterpret_cast<double2*>(a);
   double2* nxt = reinterpret_cast<double2*>(b);
-  // Overlap: the temporally blocked launch is split into the band of tile
-  // rows that read no ghost row (owned rows [band, ny_local - band), launched
-  // while the ghost rows are in flight on the comm stream) and the two edge
-  // bands (after the exchange).  band = one tile row of owned rows.
-  const int band = qwb::lattice_tb_owned_rows((int)ghost);
-  static int split_env = -1;
-  if (split_env < 0) {
-    const char* e = getenv("QWB_SLAB_SPLIT");
-    split_env = (e && *e) ? atoi(e) : 1;
-  }
-  const int ntr = band > 0 ? (int)((ny_local + band - 1) / band) : 0;   // tile rows of the slab
-  const bool split = split_env && ntr >= 3;
-  if (split && !ctx->ghost_flag) {
-    QWB_CUDA(ctx, cudaMalloc(&ctx->ghost_flag, sizeof(int)));
-    QWB_CUDA(ctx, cudaMemsetAsync(ctx->ghost_flag, 0, sizeof(int), s));
-    ctx->ghost_seq = 0;
-  }
+  // No in-kernel wait on the exchange: a persistent launch whose CTAs spin
+  // on a flag raised after an NCCL kernel on another stream deadlocks when
+  // NCCL needs more co-resident CTAs than the SMs the launch leaves free
+  // (seen at 8192 columns).  The exchange is 4 ghost rows per 4 steps, under
+  // 8 % of a launch's bytes, so it runs in stream order before the launch.
   int swaps = 0;
   for (int64_t k = 0; k < steps;) {
     const int g = (k + ghost <= steps) ? (int)ghost : 1;
-    int st;
-    if (g == (int)ghost && split) {
-      QWB_CUDA(ctx, cudaEventRecord(ctx->ev_ready, s));
-      QWB_CUDA(ctx, cudaStreamWaitEvent(cs, ctx->ev_ready, 0));
-      st = ghost_exchange_nccl(ctx, nx, ny_local, ghost, g, cur, rank_below, rank_above, cs);
-      if (st) return st;
-      raise_flag_kernel<<<1, 1, 0, cs>>>(ctx->ghost_flag, ctx->ghost_seq + 1);
-      QWB_LAUNCH_CHECK(ctx, "raise_flag_kernel");
-      QWB_CUDA(ctx, cudaEventRecord(ctx->ev_done, cs));
-      const int lr = (int)(ny_local + 2 * ghost);
-      // ONE launch: the middle tile rows first (they read no ghost row) while
-      // the exchange runs on the comm stream, then the two edge rows, whose
-      // CTAs wait for the device flag raised after the exchange
-      const int seq = ++ctx->ghost_seq;
-      const qwb::TbGeo geo{lr, (int)ghost, (int)ny_local, (int)y0, 0, 4, ntr, ctx->ghost_flag, seq};
-      st = qwb::lattice_tb_launch_geo(ctx, g, shift, s, (int)nx, (int)ny, geo, cur, nxt, marked_bits, marked_host,
-                                      n_marked);
-      if (st) return st;
-      QWB_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_done, 0));   // the comm stream's work precedes the next step
-      QWB_LAUNCH_CHECK(ctx, "lattice_tb_kernel(slab bands)");
-    } else {
-      st = ghost_exchange_nccl(ctx, nx, ny_local, ghost, g, cur, rank_below, rank_above, s);
-      if (st) return st;
-      st = qwb_slab_advance_local(ctx, nx, ny, y0, ny_local, ghost, shift, marked_bits, marked_host, n_marked,
-                                  reinterpret_cast<qwb_z*>(cur), reinterpret_cast<qwb_z*>(nxt), g, stream);
-      if (st) return st;
-    }
+    int st = ghost_exchange_nccl(ctx, nx, ny_local, ghost, g, cur, rank_below, rank_above, s);
+    if (st) return st;
+    st = qwb_slab_advance_local(ctx, nx, ny, y0, ny_local, ghost, shift, marked_bits, marked_host, n_marked,
+                                reinterpret_cast<qwb_z*>(cur), reinterpret_cast<qwb_z*>(nxt), g, stream);
+    if (st) return st;
     double2* t = cur;
     cur = nxt;
     nxt = t;

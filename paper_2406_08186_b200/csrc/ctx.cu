@@ -106,8 +106,6 @@ int qwb_init(int device, qwb_ctx** out) {
   c->comm_stream = nullptr;
   c->ev_ready = nullptr;
   c->ev_done = nullptr;
-  c->ghost_flag = nullptr;
-  c->ghost_seq = 0;
   e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaMallocHost(&c->pinned, 4096);
   if (e != cudaSuccess) {
@@ -132,8 +130,6 @@ int qwb_shutdown(qwb_ctx* ctx) {
   if (ctx->comm) qwb_comm_destroy(ctx);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
-  if (ctx->ghost_flag) cudaFree(ctx->ghost_flag);
-  ctx->ghost_flag = nullptr;
   ctx->ws = nullptr;
   ctx->pinned = nullptr;
   ctx->stopped = true;

@@ -510,7 +510,7 @@ int qwb_slab_advance_local(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int
     return QWB_OK;
   }
   if (nsteps != ghost) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "nsteps must be 1 or the ghost depth");
-  const qwb::TbGeo geo{(int)(ny_local + 2 * ghost), (int)ghost, (int)ny_local, (int)y0, 0, 0, 0, nullptr, 0};
+  const qwb::TbGeo geo{(int)(ny_local + 2 * ghost), (int)ghost, (int)ny_local, (int)y0, 0};
   st = qwb::lattice_tb_launch_geo(ctx, (int)ghost, shift, s, (int)nx, (int)ny, geo, x, y, marked_bits,
                                   marked_host, n_marked);
   if (st) return st;

@@ -25,8 +25,7 @@
 //
 // Regions wrap around the torus (modular global coordinates): any nx, ny >= 3.
 // The same kernel runs on multi-GPU y-slabs with ghost state rows (SLAB,
-// TbGeo): owned rows only, no y-wrap, optionally waiting on a device flag
-// before the tiles that read the ghost rows (comm.cu qwb_slab_run_fused).
+// TbGeo): owned rows only, no y-wrap (comm.cu qwb_slab_run_fused).
 // Default tile: 16 warps x 4 rows (32 x 64 region), T = 4.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -213,7 +212,7 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
   double2* trbuf = reinterpret_cast<double2*>(tbar + 2);          // [T][8][4] traced amplitudes (TRACE)
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * 32 + tx;
-  if (!SLAB) geo = TbGeo{ny, 0, ny, 0, 1, 0, 0, nullptr, 0};   // compile-time constants for the torus
+  if (!SLAB) geo = TbGeo{ny, 0, ny, 0, 1};   // compile-time constants for the torus
   // Tiles whose region lies inside the torus (no wrap) load all four planes
   // with ONE tensor TMA (box [4][RY][32] complex128) completing on a stage
   // mbarrier; regions that wrap use per-thread cp.async.
@@ -255,26 +254,6 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
       ++r;
     }
   };
-  // mid-first slab launches: virtual tile row r < ntr - 2 is row r + 1, then
-  // the edge rows 0 and ntr - 1 (which wait for the ghost rows)
-  const bool midfirst = SLAB && geo.ntr >= 3;
-  auto rmap = [&](int r) {
-    if (!midfirst) return r;
-    return r < geo.ntr - 2 ? r + 1 : (r == geo.ntr - 2 ? 0 : geo.ntr - 1);
-  };
-  bool ghosts_ready = !midfirst || geo.ready == nullptr;
-  auto need_ghosts = [&](int vr) {   // CTA-uniform call sites only
-    if (ghosts_ready || vr < geo.ntr - 2) return;
-    if (tid == 0) {
-      int v;
-      do {
-        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(geo.ready) : "memory");
-      } while (v < geo.ready_val);
-      asm volatile("fence.proxy.async.global;\n" ::: "memory");   // TMA reads after the acquire
-    }
-    __syncthreads();
-    ghosts_ready = true;
-  };
   auto prefetch = [&](double2* stage, int tcol, int trow) {
     const int bx = tcol * OX - T + tx;
     const int by = geo.own0 + trow * OY - T + ty * V;   // local buffer row
@@ -303,12 +282,11 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
   for (int k = 0; k < S::NSTAGE; ++k) {
     if (ptile < ntiles) {
       double2* st = stage0 + (size_t)k * 4 * S::REG;
-      need_ghosts(prow);
-      if (tma_ok(pcol, rmap(prow))) {
-        tma_load(st, tbar + k, pcol, rmap(prow));
+      if (tma_ok(pcol, prow)) {
+        tma_load(st, tbar + k, pcol, prow);
         (k ? f1 : f0) = true;
       } else {
-        prefetch(st, pcol, rmap(prow));
+        prefetch(st, pcol, prow);
       }
     }
     cp_commit();
@@ -320,7 +298,7 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
     double2* stage = stage0 + (size_t)k * 4 * S::REG;
     // x0: global column of the tile's first owned column; y0: unwrapped
     // global row of its first owned row; lyb: its local buffer row
-    const int trow_now = rmap(trow);
+    const int trow_now = trow;
     const int x0 = tcol * OX, y0 = geo.ybase + trow_now * OY, lyb = geo.own0 + trow_now * OY;
     advance(tcol, trow);
     const int gx = wrapc(x0 - T + tx, nx);
@@ -347,12 +325,11 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
     __syncthreads();
     if (k) f1 = false; else f0 = false;
     if (ptile < ntiles) {   // into the stage just consumed
-      need_ghosts(prow);
-      if (tma_ok(pcol, rmap(prow))) {
-        tma_load(stage, tbar + k, pcol, rmap(prow));
+      if (tma_ok(pcol, prow)) {
+        tma_load(stage, tbar + k, pcol, prow);
         if (k) f1 = true; else f0 = true;
       } else {
-        prefetch(stage, pcol, rmap(prow));
+        prefetch(stage, pcol, prow);
       }
     }
     cp_commit();
@@ -423,11 +400,10 @@ int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const TbGeo& geo, 
                 double2* out, const uint32_t* bits, const MarkedList& mk, const TraceList& tr) {
   using Sh = TbShape<BY, V>;
   constexpr int OX = Sh::RX - 2 * T, OY = Sh::RY - 2 * T;
-  const int tiles_x = (nx + OX - 1) / OX, tiles_y = geo.ntr >= 3 ? geo.ntr : (geo.nown + OY - 1) / OY;
+  const int tiles_x = (nx + OX - 1) / OX, tiles_y = (geo.nown + OY - 1) / OY;
   const int ntiles = tiles_x * tiles_y;
   const size_t smem = Sh::smem_bytes();
-  const int cap = ctx->num_sms - geo.spare_sms > 1 ? ctx->num_sms - geo.spare_sms : 1;
-  const int grid = ntiles < cap ? ntiles : cap;
+  const int grid = ntiles < ctx->num_sms ? ntiles : ctx->num_sms;
   // tensor map of the input planes for the TMA tile loads: doubles
   // [4][lrows][2 nx] (lrows = ny on the torus, the slab's buffer rows), box
   // [4][RY][64] = one stage
@@ -709,7 +685,7 @@ int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx
                       const double2* in, double2* out, const uint32_t* bits,
                       const int64_t* marked_host, int64_t n_marked,
                       const int64_t* trace_vertices_host, int n_trace, double* trace) {
-  const TbGeo geo{ny, 0, ny, 0, 1, 0, 0, nullptr, 0};
+  const TbGeo geo{ny, 0, ny, 0, 1};
   return tb_launch_impl(ctx, depth, shift, s, nx, ny, geo, in, out, bits, marked_host, n_marked,
                         trace_vertices_host, n_trace, trace);
 }

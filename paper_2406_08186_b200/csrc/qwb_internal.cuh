@@ -24,9 +24,6 @@ struct qwb_ctx {
   int nranks, rank;
   cudaStream_t comm_stream;
   cudaEvent_t ev_ready, ev_done;
-  // device flag raised on the comm stream when a slab's ghost rows landed
-  int* ghost_flag;
-  int ghost_seq;
 };
 
 namespace qwb {

@@ -232,13 +232,6 @@ int lattice_check_shift(qwb_ctx* ctx, int shift);
 // >= T ghost rows each side holding the neighbours' state (no wrap).
 struct TbGeo {
   int lrows, own0, nown, ybase, wrap;
-  int spare_sms;    // SMs left free (for NCCL kernels running alongside)
-  // ntr > 0 (slabs): the launch covers ntr tile rows, the middle ones first; the
-  // two edge rows read ghost rows and wait until *ready >= ready_val (set on
-  // the comm stream once the ghost exchange has landed)
-  int ntr;
-  const int* ready;
-  int ready_val;
 };
 int lattice_tb_depth(int64_t nx, int64_t ny, int64_t n_marked);
 int lattice_kind();   // 1 = CTA-tile kernel, 0 = wavefront kernel
