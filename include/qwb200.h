@@ -286,6 +286,25 @@ int qwb_taylor_evolve_hypercube_shards_local(qwb_ctx* ctx, int dim, int log2_sha
 int qwb_hypercube_apply(qwb_ctx* ctx, int dim, double gamma, const uint32_t* marked_bits,
                         const qwb_z* x, qwb_z* y, void* stream);
 
+/* ---- distribution sinks (host; reference cli.py:398-432) ----------------
+ * Text of a probability record exactly as the reference's JSON / CSV /
+ * frames sinks write it (Python float repr: shortest round-trip digits,
+ * fixed notation for -4 < decpt <= 16, else d.ddde+XX).  Host-only helpers:
+ * no context, no device memory; threads > 1 splits the record.
+ * qwb_format_f64_repr: one value into out (>= 32 bytes), returns its length;
+ *   json = 1 spells non-finite values NaN / Infinity / -Infinity, else
+ *   nan / inf / -inf.
+ * qwb_format_json_floats: "p0,p1,...,p{n-1}" (the body of a "p" list,
+ *   cli.py:403-405); returns the length, or -1 if cap is too small
+ *   (n * 25 bytes always suffices).
+ * qwb_format_csv_rows: one line "<prefix><vertex0+i>,<p[i]>\n" per item i (prefix
+ *   "k,t," for the csv sink, cli.py:413-416; "" for a frame file, 425-428);
+ *   returns the length or -1 (n * (prefix_len + 47) bytes always suffice). */
+int qwb_format_f64_repr(double x, int json, char* out);
+int64_t qwb_format_json_floats(const double* p, int64_t n, char* out, int64_t cap, int threads);
+int64_t qwb_format_csv_rows(const double* p, int64_t n, int64_t vertex0, const char* prefix, int64_t prefix_len,
+                            char* out, int64_t cap, int threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -34,8 +34,19 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found: cannot build libqwb200.so")
 
 
+CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-g", "-I" + os.path.join(ROOT, "include")]
+
+
 def sources() -> list[str]:
-    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
+    """CUDA sources (nvcc) and host-only C++ sources (g++)."""
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp")))
+
+
+def cxx() -> str:
+    for cand in (os.environ.get("CXX"), shutil.which("g++")):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("g++ not found: cannot build libqwb200.so")
 
 
 def _stale(obj: str, src: str) -> bool:
@@ -52,12 +63,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ_DIR, exist_ok=True)
     nv = nvcc()
     srcs = sources()
-    objs = [os.path.join(OBJ_DIR, os.path.basename(s)[:-3] + ".o") for s in srcs]
+    objs = [os.path.join(OBJ_DIR, os.path.splitext(os.path.basename(s))[0] + ".o") for s in srcs]
     todo = [(s, o) for s, o in zip(srcs, objs) if force or _stale(o, s)]
 
     def compile_one(so):
         s, o = so
-        cmd = [nv] + NVCC_FLAGS + ["-c", s, "-o", o]
+        if s.endswith(".cpp"):
+            cmd = [cxx()] + CXX_FLAGS + ["-c", s, "-o", o]
+        else:
+            cmd = [nv] + NVCC_FLAGS + ["-c", s, "-o", o]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {s}:\n{r.stdout}\n{r.stderr}")

@@ -106,8 +106,12 @@ SIGNATURES = {
     "qwb_taylor_evolve_hypercube": [_vp, _i32, _dbl, _vp, _vp, _vp, _i64, _dbl, _dbl, _i32, _p_int,
                                     _vp],
     "qwb_hypercube_apply": [_vp, _i32, _dbl, _vp, _vp, _vp, _vp],
+    "qwb_format_f64_repr": [_dbl, _i32, _vp],
+    "qwb_format_json_floats": [_vp, _i64, _vp, _i64, _i32],
+    "qwb_format_csv_rows": [_vp, _i64, _i64, C.c_char_p, _i64, _vp, _i64, _i32],
 }
-_RESTYPES = {"qwb_last_error": C.c_char_p, "qwb_version": C.c_char_p}
+_RESTYPES = {"qwb_last_error": C.c_char_p, "qwb_version": C.c_char_p,
+             "qwb_format_json_floats": C.c_int64, "qwb_format_csv_rows": C.c_int64}
 
 _lock = threading.Lock()
 _lib = None
