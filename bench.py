@@ -96,7 +96,9 @@ class Clocks:
         self.lines = []
         self.t = None
 
-    def start(self):
+    def start(self, wait_s: float = 5.0):
+        """Start polling every 50 ms; wait for the first sample (nvidia-smi
+        takes ~0.5 s to start) so that a short timed region is covered."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-i",
@@ -104,12 +106,19 @@ class Clocks:
                 text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t_end = time.time() + wait_s
+            while not self.lines and time.time() < t_end:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self):
+        """Start of the timed region (samples before it are the warm-up's)."""
+        self.t0 = time.time()
 
     def stop(self):
         if self.proc is None:
@@ -120,8 +129,16 @@ class Clocks:
         except Exception:
             self.proc.kill()
         self.t.join(timeout=2)
+        t0 = getattr(self, "t0", None)
+        timed = [ln for t, ln in self.lines if t0 is None or t >= t0]
+        # a timed region shorter than the polling period: the samples of the
+        # warm-up steps just before it (same kernels, GPU busy) stand in
+        window = "timed"
+        if not timed:
+            timed = [ln for _, ln in self.lines[-5:]]
+            window = "warm-up + timed (region shorter than the 50 ms poll)"
         sm, smax, reasons = [], [], set()
-        for ln in self.lines:
+        for ln in timed:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -135,7 +152,7 @@ class Clocks:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "window": window}
 
 
 # ---------------------------------------------------------------------------
@@ -290,14 +307,15 @@ def run_b200(args):
     # ---- device-resident timed region: runner.advance(walk) per bench step
     runner.load(x)
     stream = torch.cuda.current_stream(dev)
+    clocks = Clocks(local)
+    clocks.start()
     for _ in range(args.warmup):
         runner.advance(walk)
     torch.cuda.synchronize(dev)
-    clocks = Clocks(local)
-    clocks.start()
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
+    clocks.mark()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
