@@ -377,17 +377,19 @@ def search_trace(engine: Engine, spec: CoinedSpec, steps: int, psi0: WalkState,
     r = _LatticeRunner(engine, spec)
     r.load(x)
     trace = torch.empty((steps + 1, len(marked)), dtype=torch.float64, device=engine.torch_device)
-    dists = {}
     p = torch.empty(g.n, dtype=torch.float64, device=engine.torch_device)
     done = 0
     every = distribution_every if distribution_every > 0 else steps + 1
+    # saved distributions download beside the steps that follow them
+    keys = list(range(every, steps + 1, every))
+    pipe = SnapshotPipe(engine, g.n, max(2, len(keys)), dtype=torch.float64)
     while done < steps:
         chunk = min(steps - done, every - (done % every))
         r.advance(chunk, trace[done:], marked)
         done += chunk
         if done % every == 0:
-            r.probability(p)
-            dists[done] = to_host(p).copy()
+            pipe.capture(r.probability)
+    dists = {k: arr for k, (arr, _owner) in zip(keys, pipe.results())}
     # p(marked) of the final state
     r.probability(p)
     last = p[list(marked)]
