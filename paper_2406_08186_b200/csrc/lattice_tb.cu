@@ -201,7 +201,7 @@ template <int SHIFT, bool MARKED, int T, int BY, int V, bool TRACE, bool SLAB>
 __global__ void __launch_bounds__(32 * BY, 1)
 lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, double2* __restrict__ out,
                   const uint32_t* __restrict__ bits, MarkedList mk, TraceList tr, int tiles_x,
-                  int ntiles, const __grid_constant__ CUtensorMap imap, int use_tma) {
+                  int ntiles, int tile0, const __grid_constant__ CUtensorMap imap, int use_tma) {
   using S = TbShape<BY, V>;
   constexpr int OX = S::RX - 2 * T, OY = S::RY - 2 * T;   // exact (owned) block
   extern __shared__ double2 sm[];
@@ -271,7 +271,7 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
     }
   };
 
-  int tile = blockIdx.x;
+  int tile = blockIdx.x + tile0;   // tile0 > 0: a launch over tiles [tile0, ntiles) only
   if (tile >= ntiles) return;
   int tcol = tile % tiles_x, trow = tile / tiles_x;
   // (pcol, prow): the tile the next prefetch loads, NSTAGE - 1 tiles ahead of (tcol, trow)
@@ -429,14 +429,15 @@ int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const TbGeo& geo, 
                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     }
   }
-  auto go = [&](auto kernel, bool* configured) -> int {
+  auto go = [&](auto kernel, bool* configured, int grid_ = 0, int tile0 = 0, int ntiles_ = 0) -> int {
     const int dev = ctx->device & 255;
     if (!configured[dev]) {
       cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return qwb::cuda_status(ctx, e, "cudaFuncSetAttribute(lattice_tb)");
       configured[dev] = true;
     }
-    kernel<<<grid, dim3(32, BY), smem, s>>>(nx, ny, geo, in, out, bits, mk, tr, tiles_x, ntiles, imap, use_tma);
+    kernel<<<grid_ ? grid_ : grid, dim3(32, BY), smem, s>>>(nx, ny, geo, in, out, bits, mk, tr, tiles_x,
+                                                            ntiles_ ? ntiles_ : ntiles, tile0, imap, use_tma);
     return QWB_OK;
   };
   static bool conf_plain[256] = {}, conf_trace[256] = {}, conf_slab[256] = {};   // per instantiation, device
@@ -448,8 +449,27 @@ int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const TbGeo& geo, 
       QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "slab kernels exist for T = %d on 32x64 regions only", kSlabDepth);
     }
   }
-  if (tr.n > 0) return go(lattice_tb_kernel<SHIFT, MARKED, T, BY, V, true, false>, conf_trace);
-  return go(lattice_tb_kernel<SHIFT, MARKED, T, BY, V, false, false>, conf_plain);
+  static int trace_split = env_int("QWB_LATTICE_TRACE_SPLIT", 1);
+  if (tr.n > 0 && !trace_split) return go(lattice_tb_kernel<SHIFT, MARKED, T, BY, V, true, false>, conf_trace);
+  int st = go(lattice_tb_kernel<SHIFT, MARKED, T, BY, V, false, false>, conf_plain);
+  if (st || tr.n == 0) return st;
+  // Traced run: the plain launch above advanced every tile; the tiles that own
+  // a traced vertex are then recomputed from the same input (still intact: the
+  // output is the other buffer) by the TRACE instantiation, one CTA each, which
+  // records the traced vertices' per-level p and stores the same owned values
+  // again.  Keeps the trace's registers and checks out of the full launch.
+  int done_tiles[8];
+  int nd = 0;
+  for (int k = 0; k < tr.n; ++k) {
+    const int t = (tr.y[k] / OY) * tiles_x + tr.x[k] / OX;
+    bool seen = false;
+    for (int j = 0; j < nd; ++j) seen |= done_tiles[j] == t;
+    if (seen) continue;
+    done_tiles[nd++] = t;
+    st = go(lattice_tb_kernel<SHIFT, MARKED, T, BY, V, true, false>, conf_trace, 1, t, t + 1);
+    if (st) return st;
+  }
+  return QWB_OK;
 }
 
 template <int T, int BY, int V>
