@@ -709,11 +709,15 @@ void launch_stream(const HcStream& op, cudaStream_t s, int64_t n, const double2*
 int launch_term(const HcStream& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
                 const double2* ain, double2* acc, double s_k, const int* flags, double* partial) {
   // QWB_HC_STREAM = CONS/256 * 10000 + NS * 100 + SPLIT (tuning knob; measured at
-  // dim 22: 601 173, 20601 157, 20801 151-154 us/term)
+  // dim 22: 601 173, 20601 157, 20801 143-144.5, 21001 139.6, 21201 140.7,
+  // 20804 166 us/term)
   switch (op.variant) {
     case 601: launch_stream<6, 1, 256>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
     case 20601: launch_stream<6, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
-    default: launch_stream<8, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+    case 21201: launch_stream<12, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+    case 20804: launch_stream<8, 4, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+    case 20801: launch_stream<8, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+    default: launch_stream<10, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
   }
   return op.grid;
 }
@@ -936,7 +940,7 @@ int hc_stream_base(qwb_ctx* ctx, int dim, int S, double gamma, const uint32_t* b
   static int variant = -1;
   if (variant < 0) {
     const char* e = getenv("QWB_HC_STREAM");
-    variant = (e && *e) ? atoi(e) : 20801;
+    variant = (e && *e) ? atoi(e) : 21001;
   }
   const int64_t ntiles = 1LL << (dim - S - hcs::LB);
   *op = HcStream{};
