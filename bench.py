@@ -346,11 +346,16 @@ def run_b200(args):
             per_walk = walk
             kernel = "lattice_step_kernel<flipflop>"
     elif runner.ghost:
-        # fused slabs: per G-step launch the middle band beside the ghost-row
-        # exchange, then the two edge bands; remainder steps one at a time
-        depth = runner.ghost
-        per_walk = 3 * (walk // depth) + walk % depth
-        kernel = f"lattice_tb_kernel<flipflop, T={depth}, 32x64 region> on y-slabs with {depth} ghost rows"
+        # fused slabs: per exchange of G ghost rows, G / T launches of T steps
+        # (G = 2T: an extended launch, then an owned one); remainder: one
+        # T-step launch, then single steps
+        G = runner.ghost
+        depth = G // 2 if G >= 8 else G
+        n2 = walk // G if G == 2 * depth else 0
+        rem = walk - n2 * G
+        per_walk = 2 * n2 + rem // depth + rem % depth
+        kernel = (f"lattice_tb_kernel<flipflop, T={depth}, 32x64 region> on y-slabs with {G} ghost rows "
+                  f"({G // depth} launches per exchange)")
     else:
         depth = 0
         per_walk = 2 * walk

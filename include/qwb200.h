@@ -182,12 +182,16 @@ int qwb_slab_probability(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64
 int qwb_slab_step(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int shift,
                   const uint32_t* marked_bits, const qwb_z* in, qwb_z* out, int part, void* stream);
 /* Fused (temporally blocked) slabs: G = qwb_slab_ghost_rows(...) ghost rows
- * each side (0: not available, use the 1-extra-row functions above); planes
- * hold 4 x nx x (ny_local + 2G) qwb_z, owned rows are local rows [G, G+ny_local).
- * qwb_slab_run_fused: G coined steps per launch of the temporally blocked kernel
- * on the owned rows, preceded by an NCCL exchange of G state rows per plane
- * with each y-neighbour; remainder steps one at a time (1-row exchange).  The
- * same arithmetic as one GPU: bitwise equal.                                  */
+ * each side (2T when the thinnest slab holds 2T rows, else T, 0: not
+ * available, use the 1-extra-row functions above; T = 4, the slab depth);
+ * planes hold 4 x nx x (ny_local + 2G) qwb_z, owned rows are local rows
+ * [G, G+ny_local).
+ * qwb_slab_run_fused: per NCCL exchange of G state rows per plane with each
+ * y-neighbour, G coined steps as G / T launches of the temporally blocked
+ * kernel (with G = 2T the first covers the owned rows extended by T rows each
+ * side, the second the owned rows); remainder steps as one T-step launch
+ * (T-row exchange) and single pull steps (1-row exchange).  The same
+ * arithmetic as one GPU: bitwise equal.                                       */
 int qwb_slab_ghost_rows(int64_t nx, int64_t ny, int64_t ny_local, int64_t n_marked, int* ghost_host);
 int qwb_slab_to_planes_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
                          const qwb_z* arcs, qwb_z* planes, void* stream);
@@ -195,10 +199,11 @@ int qwb_slab_from_planes_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int
                            const qwb_z* planes, qwb_z* arcs, void* stream);
 int qwb_slab_probability_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
                            const qwb_z* planes, double* p, void* stream);
-/* one launch without exchange: nsteps = ghost (temporally blocked) or 1 (pull step) */
+/* one launch without exchange: nsteps = T (temporally blocked, over the owned
+ * rows extended by ext rows each side; ghost - ext >= T) or 1 (pull step, ext 0) */
 int qwb_slab_advance_local(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
                            int shift, const uint32_t* marked_bits, const int64_t* marked_host, int64_t n_marked,
-                           const qwb_z* in, qwb_z* out, int nsteps, void* stream);
+                           const qwb_z* in, qwb_z* out, int nsteps, int ext, void* stream);
 int qwb_slab_run_fused(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
                        int shift, const uint32_t* marked_bits, const int64_t* marked_host, int64_t n_marked,
                        qwb_z* a, qwb_z* b, int64_t steps, int rank_below, int rank_above, int* final_in_b_host,

@@ -83,7 +83,8 @@ SIGNATURES = {
     "qwb_slab_to_planes_g": [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp],
     "qwb_slab_from_planes_g": [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp],
     "qwb_slab_probability_g": [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp],
-    "qwb_slab_advance_local": [_vp, _i64, _i64, _i64, _i64, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _i32, _vp],
+    "qwb_slab_advance_local": [_vp, _i64, _i64, _i64, _i64, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _i32, _i32,
+                               _vp],
     "qwb_slab_run_fused": [_vp, _i64, _i64, _i64, _i64, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _i64, _i32, _i32,
                            _p_int, _vp],
     "qwb_slab_ghost_exchange_local": [_vp, _i64, _i64, _i32, _p_i64, C.POINTER(_vp), _i32, _vp],

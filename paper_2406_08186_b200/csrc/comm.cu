@@ -314,18 +314,34 @@ int qwb_slab_run_fused(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t
   // NCCL needs more co-resident CTAs than the SMs the launch leaves free
   // (seen at 8192 columns).  The exchange is 4 ghost rows per 4 steps, under
   // 8 % of a launch's bytes, so it runs in stream order before the launch.
+  // G = 2T: per exchange of 2T rows, one launch over the owned rows extended
+  // by T rows each side, then one over the owned rows; G = T: one launch per
+  // exchange of T rows; the remainder as single pull steps (1-row exchange)
+  const int T = qwb::lattice_slab_depth(ghost >= 8 ? (int)ghost / 2 : (int)ghost);
+  if (T == 0 || (ghost != T && ghost != 2 * T))
+    QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "ghost rows must be the slab depth or twice it");
   int swaps = 0;
-  for (int64_t k = 0; k < steps;) {
-    const int g = (k + ghost <= steps) ? (int)ghost : 1;
-    int st = ghost_exchange_nccl(ctx, nx, ny_local, ghost, g, cur, rank_below, rank_above, s);
-    if (st) return st;
-    st = qwb_slab_advance_local(ctx, nx, ny, y0, ny_local, ghost, shift, marked_bits, marked_host, n_marked,
-                                reinterpret_cast<qwb_z*>(cur), reinterpret_cast<qwb_z*>(nxt), g, stream);
-    if (st) return st;
+  auto launch = [&](int nsteps, int ext) -> int {
+    const int st = qwb_slab_advance_local(ctx, nx, ny, y0, ny_local, ghost, shift, marked_bits, marked_host,
+                                          n_marked, reinterpret_cast<qwb_z*>(cur), reinterpret_cast<qwb_z*>(nxt),
+                                          nsteps, ext, stream);
     double2* t = cur;
     cur = nxt;
     nxt = t;
     ++swaps;
+    return st;
+  };
+  for (int64_t k = 0; k < steps;) {
+    const int g = (ghost == 2 * T && k + 2 * T <= steps) ? 2 * T : (k + T <= steps ? T : 1);
+    int st = ghost_exchange_nccl(ctx, nx, ny_local, ghost, g, cur, rank_below, rank_above, s);
+    if (st) return st;
+    if (g == 2 * T) {
+      st = launch(T, T);
+      if (!st) st = launch(T, 0);
+    } else {
+      st = launch(g, 0);
+    }
+    if (st) return st;
     k += g;
   }
   if (final_in_b_host) *final_in_b_host = swaps & 1;

@@ -479,19 +479,25 @@ int qwb_slab_probability_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int
 }
 
 int qwb_slab_ghost_rows(int64_t nx, int64_t ny, int64_t ny_local, int64_t n_marked, int* ghost_host) {
-  int d = qwb::lattice_slab_depth(qwb::lattice_tb_depth(nx, ny, n_marked));
-  if (d < 2 || ny_local < d || nx < 64) d = 0;
-  if (ghost_host) *ghost_host = d;
+  // G = 2T ghost rows (two temporally blocked launches per exchange) when the
+  // thinnest slab holds them, else T (one launch per exchange), else 0
+  const int d = qwb::lattice_slab_depth(qwb::lattice_tb_depth(nx, ny, n_marked));
+  int g = 0;
+  if (d >= 2 && nx >= 64 && ny_local >= d) g = ny_local >= 2 * d ? 2 * d : d;
+  if (ghost_host) *ghost_host = g;
   return QWB_OK;
 }
 
-// One launch on a ghost-row slab, no exchange: nsteps == ghost runs the
-// temporally blocked kernel over the owned rows (reads the ghost rows' state),
-// nsteps == 1 one pull step (owned rows plus one ghost row each side pushed,
-// so every owned output receives all four pushes).
+// One launch on a ghost-row slab, no exchange.  nsteps == 1: one pull step
+// (owned rows plus one ghost row each side pushed, so every owned output
+// receives all four pushes).  nsteps == T (the slab depth): the temporally
+// blocked kernel over the owned rows extended by ext rows each side (global
+// rows [y0 - ext, y0 + ny_local + ext)); needs ghost - ext >= T valid ghost
+// rows each side.  With G = 2T, ext = T then ext = 0 advance 2T steps per
+// exchange of 2T rows.
 int qwb_slab_advance_local(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
                            int shift, const uint32_t* marked_bits, const int64_t* marked_host, int64_t n_marked,
-                           const qwb_z* in, qwb_z* out, int nsteps, void* stream) {
+                           const qwb_z* in, qwb_z* out, int nsteps, int ext, void* stream) {
   QWB_BEGIN(ctx);
   Geom g;
   int st = qwb::lattice_slab_geom_g(ctx, nx, ny, y0, ny_local, ghost, &g);
@@ -504,15 +510,19 @@ int qwb_slab_advance_local(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int
   const double2* x = reinterpret_cast<const double2*>(in);
   double2* y = reinterpret_cast<double2*>(out);
   if (nsteps == 1) {
+    if (ext != 0) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "pull steps cover the owned rows only (ext = 0)");
     TraceArgs tr{};
     qwb::lattice_launch(shift, s, g, Rows{(int)ghost - 1, 1, (int)ny_local + 2}, x, y, marked_bits, nullptr, 0, tr);
     QWB_LAUNCH_CHECK(ctx, "lattice_step_kernel(ghost slab)");
     return QWB_OK;
   }
-  if (nsteps != ghost) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "nsteps must be 1 or the ghost depth");
-  const qwb::TbGeo geo{(int)(ny_local + 2 * ghost), (int)ghost, (int)ny_local, (int)y0, 0};
-  st = qwb::lattice_tb_launch_geo(ctx, (int)ghost, shift, s, (int)nx, (int)ny, geo, x, y, marked_bits,
-                                  marked_host, n_marked);
+  const int T = qwb::lattice_slab_depth(nsteps);
+  if (T == 0 || nsteps != T) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "nsteps must be 1 or the slab depth");
+  if (ext < 0 || ghost - ext < T)
+    QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "ext = %d leaves fewer than %d ghost rows", ext, T);
+  const qwb::TbGeo geo{(int)(ny_local + 2 * ghost), (int)ghost - ext, (int)ny_local + 2 * ext, (int)y0 - ext, 0};
+  st = qwb::lattice_tb_launch_geo(ctx, T, shift, s, (int)nx, (int)ny, geo, x, y, marked_bits, marked_host,
+                                  n_marked);
   if (st) return st;
   QWB_LAUNCH_CHECK(ctx, "lattice_tb_kernel(ghost slab)");
   return QWB_OK;

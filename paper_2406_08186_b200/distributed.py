@@ -491,7 +491,7 @@ def slab_ghost_rows(nx: int, ny: int, world: int, n_marked: int) -> int:
 def emulate_slabs_fused(engine: Engine, nx: int, ny: int, world: int, psi_arcs: np.ndarray, steps: int,
                         shift: str = "flipflop", marked=()):
     """The fused slab decomposition (G ghost state rows, G steps per
-    temporally blocked launch, single pull steps for the remainder) for
+    exchange as G / T temporally blocked launches, single pull steps for the remainder) for
     `world` slabs on ONE device, exchanging ghost rows with device copies
     exactly as qwb_slab_run_fused's NCCL group does.  Returns the full arc
     state.  Test hook for the multi-GPU path."""
@@ -519,15 +519,27 @@ def emulate_slabs_fused(engine: Engine, nx: int, ny: int, world: int, psi_arcs: 
         cur.append(a)
         nxt.append(b)
     nl = N.i64_array([r for (_, r) in parts])
-    k = 0
-    while k < steps:
-        g = G if k + G <= steps else 1
-        ptrs = (C.c_void_p * world)(*[N.ptr(t) for t in cur])
-        engine.call("qwb_slab_ghost_exchange_local", nx, G, g, nl, ptrs, world, engine.stream())
+    T = G // 2 if G >= 8 else G   # slab depth: G = 2T or G = T (qwb_slab_ghost_rows)
+
+    def launch(nsteps, ext):
+        nonlocal cur, nxt
         for i, (y0, rows) in enumerate(parts):
             engine.call("qwb_slab_advance_local", nx, ny, y0, rows, G, sh, N.ptr(bits), marr, len(marked),
-                        N.ptr(cur[i]), N.ptr(nxt[i]), g, engine.stream())
+                        N.ptr(cur[i]), N.ptr(nxt[i]), nsteps, ext, engine.stream())
         cur, nxt = nxt, cur
+
+    # qwb_slab_run_fused's schedule: 2T steps per exchange of 2T rows (an
+    # extended launch, then an owned one), else T, else single pull steps
+    k = 0
+    while k < steps:
+        g = 2 * T if (G == 2 * T and k + 2 * T <= steps) else (T if k + T <= steps else 1)
+        ptrs = (C.c_void_p * world)(*[N.ptr(t) for t in cur])
+        engine.call("qwb_slab_ghost_exchange_local", nx, G, g, nl, ptrs, world, engine.stream())
+        if g == 2 * T:
+            launch(T, T)
+            launch(T, 0)
+        else:
+            launch(g, 0)
         k += g
     out = torch.empty_like(full)
     for i, (y0, rows) in enumerate(parts):

@@ -324,7 +324,7 @@ def _ghost_worker(rank, world, port, nx, ny, G, steps, shift, marked, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,G,shift", [(2, 4, "flipflop"), (3, 3, "persistent"), (2, 2, "flipflop")])
+@pytest.mark.parametrize("world,G,shift", [(2, 4, "flipflop"), (2, 8, "flipflop"), (3, 3, "persistent"), (2, 2, "flipflop")])
 def test_gloo_multiprocess_ghost_slabs(tmp_path, world, G, shift):
     import torch.multiprocessing as mp
     nx, ny, steps, marked = 8, 18, 11, (17, 100)
