@@ -346,14 +346,12 @@ def run_b200(args):
             per_walk = walk
             kernel = "lattice_step_kernel<flipflop>"
     elif runner.ghost:
-        # fused slabs: per exchange of G ghost rows, G / T launches of T steps
-        # (G = 2T: an extended launch, then an owned one); remainder: one
-        # T-step launch, then single steps
+        # fused slabs: per exchange of G = mT ghost rows, m launches of T steps
+        # (over the owned rows extended by (m-1)T, ..., 0 rows); the last < T
+        # steps one at a time
         G = runner.ghost
-        depth = G // 2 if G >= 8 else G
-        n2 = walk // G if G == 2 * depth else 0
-        rem = walk - n2 * G
-        per_walk = 2 * n2 + rem // depth + rem % depth
+        depth = 4
+        per_walk = walk // depth + walk % depth   # one T-step launch per T steps, then single steps
         kernel = (f"lattice_tb_kernel<flipflop, T={depth}, 32x64 region> on y-slabs with {G} ghost rows "
                   f"({G // depth} launches per exchange)")
     else:

@@ -182,15 +182,14 @@ int qwb_slab_probability(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64
 int qwb_slab_step(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int shift,
                   const uint32_t* marked_bits, const qwb_z* in, qwb_z* out, int part, void* stream);
 /* Fused (temporally blocked) slabs: G = qwb_slab_ghost_rows(...) ghost rows
- * each side (2T when the thinnest slab holds 2T rows, else T, 0: not
- * available, use the 1-extra-row functions above; T = 4, the slab depth);
- * planes hold 4 x nx x (ny_local + 2G) qwb_z, owned rows are local rows
- * [G, G+ny_local).
- * qwb_slab_run_fused: per NCCL exchange of G state rows per plane with each
- * y-neighbour, G coined steps as G / T launches of the temporally blocked
- * kernel (with G = 2T the first covers the owned rows extended by T rows each
- * side, the second the owned rows); remainder steps as one T-step launch
- * (T-row exchange) and single pull steps (1-row exchange).  The same
+ * each side, G = m T with T = 4 (the slab depth), m = QWB_SLAB_GHOST_MULT (4, <= 8)
+ * and G <= the thinnest slab; 0: not available, use the 1-extra-row functions
+ * above.  Planes hold 4 x nx x (ny_local + 2G) qwb_z, owned rows are local
+ * rows [G, G+ny_local).
+ * qwb_slab_run_fused: per NCCL exchange of g = jT state rows per plane with
+ * each y-neighbour (j = m, fewer at the end), j launches of the temporally
+ * blocked kernel over the owned rows extended by (j-1)T, ..., T, 0 rows each
+ * side; the last < T steps as single pull steps (1-row exchange).  The same
  * arithmetic as one GPU: bitwise equal.                                       */
 int qwb_slab_ghost_rows(int64_t nx, int64_t ny, int64_t ny_local, int64_t n_marked, int* ghost_host);
 int qwb_slab_to_planes_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,

@@ -314,12 +314,12 @@ int qwb_slab_run_fused(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t
   // NCCL needs more co-resident CTAs than the SMs the launch leaves free
   // (seen at 8192 columns).  The exchange is 4 ghost rows per 4 steps, under
   // 8 % of a launch's bytes, so it runs in stream order before the launch.
-  // G = 2T: per exchange of 2T rows, one launch over the owned rows extended
-  // by T rows each side, then one over the owned rows; G = T: one launch per
-  // exchange of T rows; the remainder as single pull steps (1-row exchange)
-  const int T = qwb::lattice_slab_depth(ghost >= 8 ? (int)ghost / 2 : (int)ghost);
-  if (T == 0 || (ghost != T && ghost != 2 * T))
-    QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "ghost rows must be the slab depth or twice it");
+  // G = mT: per exchange of g = jT rows (j = m, fewer at the end), j launches
+  // over the owned rows extended by (j-1)T, ..., T, 0 rows each side; the last
+  // < T steps as single pull steps (1-row exchange)
+  const int T = qwb::kSlabDepth;
+  if (qwb::lattice_slab_depth(T) != T || ghost < T || ghost % T)
+    QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "ghost rows must be a multiple of the slab depth");
   int swaps = 0;
   auto launch = [&](int nsteps, int ext) -> int {
     const int st = qwb_slab_advance_local(ctx, nx, ny, y0, ny_local, ghost, shift, marked_bits, marked_host,
@@ -332,14 +332,15 @@ int qwb_slab_run_fused(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t
     return st;
   };
   for (int64_t k = 0; k < steps;) {
-    const int g = (ghost == 2 * T && k + 2 * T <= steps) ? 2 * T : (k + T <= steps ? T : 1);
-    int st = ghost_exchange_nccl(ctx, nx, ny_local, ghost, g, cur, rank_below, rank_above, s);
+    int64_t g = (steps - k) / T * T;
+    if (g > ghost) g = ghost;
+    if (g == 0) g = 1;
+    int st = ghost_exchange_nccl(ctx, nx, ny_local, ghost, (int)g, cur, rank_below, rank_above, s);
     if (st) return st;
-    if (g == 2 * T) {
-      st = launch(T, T);
-      if (!st) st = launch(T, 0);
+    if (g == 1) {
+      st = launch(1, 0);
     } else {
-      st = launch(g, 0);
+      for (int ext = (int)g - T; ext >= 0 && !st; ext -= T) st = launch(T, ext);
     }
     if (st) return st;
     k += g;

@@ -274,7 +274,7 @@ int lattice_slab_geom_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_
                         Geom* g) {
   int st = check_dims(ctx, nx, ny);
   if (st) return st;
-  if (ghost < 1 || ghost > 8) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "ghost rows must be in 1..8");
+  if (ghost < 1 || ghost > 32) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "ghost rows must be in 1..32");
   if (ny_local < ghost || ny_local < 2 || y0 < 0 || y0 + ny_local > ny)
     QWB_FAIL(ctx, QWB_E_DIMENSION, "slab rows [%lld, %lld) invalid for ny=%lld (need >= %lld rows)",
              (long long)y0, (long long)(y0 + ny_local), (long long)ny, (long long)(ghost > 2 ? ghost : 2));
@@ -479,11 +479,18 @@ int qwb_slab_probability_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int
 }
 
 int qwb_slab_ghost_rows(int64_t nx, int64_t ny, int64_t ny_local, int64_t n_marked, int* ghost_host) {
-  // G = 2T ghost rows (two temporally blocked launches per exchange) when the
-  // thinnest slab holds them, else T (one launch per exchange), else 0
+  // G = m T ghost rows (m temporally blocked launches per exchange), m <= 4
+  // (QWB_SLAB_GHOST_MULT) and G <= the thinnest slab; 0: not available
   const int d = qwb::lattice_slab_depth(qwb::lattice_tb_depth(nx, ny, n_marked));
   int g = 0;
-  if (d >= 2 && nx >= 64 && ny_local >= d) g = ny_local >= 2 * d ? 2 * d : d;
+  if (d >= 2 && nx >= 64 && ny_local >= d) {
+    const char* e = getenv("QWB_SLAB_GHOST_MULT");
+    int m = (e && *e) ? atoi(e) : 4;
+    if (m < 1) m = 1;
+    if (m > 8) m = 8;
+    if (m > ny_local / d) m = (int)(ny_local / d);
+    g = m * d;
+  }
   if (ghost_host) *ghost_host = g;
   return QWB_OK;
 }
@@ -493,8 +500,8 @@ int qwb_slab_ghost_rows(int64_t nx, int64_t ny, int64_t ny_local, int64_t n_mark
 // receives all four pushes).  nsteps == T (the slab depth): the temporally
 // blocked kernel over the owned rows extended by ext rows each side (global
 // rows [y0 - ext, y0 + ny_local + ext)); needs ghost - ext >= T valid ghost
-// rows each side.  With G = 2T, ext = T then ext = 0 advance 2T steps per
-// exchange of 2T rows.
+// rows each side.  With G = mT, ext = (m-1)T, ..., T, 0 advance mT steps per
+// exchange of mT rows.
 int qwb_slab_advance_local(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
                            int shift, const uint32_t* marked_bits, const int64_t* marked_host, int64_t n_marked,
                            const qwb_z* in, qwb_z* out, int nsteps, int ext, void* stream) {

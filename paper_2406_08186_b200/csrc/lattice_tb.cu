@@ -78,7 +78,7 @@ __device__ __forceinline__ double2 shfl_up2(double2 v) {
   return make_double2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
 }
 
-constexpr int kSlabDepth = 4;   // the slab (ghost-row) kernels are built for this depth
+using qwb::kSlabDepth;
 constexpr size_t kTraceRecBytes = 6 * 8 * 4 * sizeof(double2);   // [T <= 6][8 vertices][4 planes]
 
 template <int BY, int V>

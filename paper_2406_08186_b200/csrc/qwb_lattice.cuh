@@ -230,6 +230,7 @@ int lattice_check_shift(qwb_ctx* ctx, int shift);
 // rows [own0, own0 + nown) = global rows [ybase, ybase + nown).  wrap = 1:
 // the buffer is the whole torus (rows wrap inside it); wrap = 0: a slab with
 // >= T ghost rows each side holding the neighbours' state (no wrap).
+constexpr int kSlabDepth = 4;   // the slab (ghost-row) tile kernels are built for this depth
 struct TbGeo {
   int lrows, own0, nown, ybase, wrap;
 };

@@ -519,7 +519,7 @@ def emulate_slabs_fused(engine: Engine, nx: int, ny: int, world: int, psi_arcs: 
         cur.append(a)
         nxt.append(b)
     nl = N.i64_array([r for (_, r) in parts])
-    T = G // 2 if G >= 8 else G   # slab depth: G = 2T or G = T (qwb_slab_ghost_rows)
+    T = 4   # the slab depth (kSlabDepth); G = m T
 
     def launch(nsteps, ext):
         nonlocal cur, nxt
@@ -528,18 +528,18 @@ def emulate_slabs_fused(engine: Engine, nx: int, ny: int, world: int, psi_arcs: 
                         N.ptr(cur[i]), N.ptr(nxt[i]), nsteps, ext, engine.stream())
         cur, nxt = nxt, cur
 
-    # qwb_slab_run_fused's schedule: 2T steps per exchange of 2T rows (an
-    # extended launch, then an owned one), else T, else single pull steps
+    # qwb_slab_run_fused's schedule: per exchange of g = jT rows, j launches
+    # over the owned rows extended by (j-1)T, ..., 0 rows; then single steps
     k = 0
     while k < steps:
-        g = 2 * T if (G == 2 * T and k + 2 * T <= steps) else (T if k + T <= steps else 1)
+        g = min(G, (steps - k) // T * T) or 1
         ptrs = (C.c_void_p * world)(*[N.ptr(t) for t in cur])
         engine.call("qwb_slab_ghost_exchange_local", nx, G, g, nl, ptrs, world, engine.stream())
-        if g == 2 * T:
-            launch(T, T)
-            launch(T, 0)
+        if g == 1:
+            launch(1, 0)
         else:
-            launch(g, 0)
+            for ext in range(g - T, -1, -T):
+                launch(T, ext)
         k += g
     out = torch.empty_like(full)
     for i, (y0, rows) in enumerate(parts):
