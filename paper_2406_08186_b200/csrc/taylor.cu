@@ -391,6 +391,33 @@ __device__ __noinline__ double2 hc_marked_row(const HcStreamArgs& a, double g, c
 
 
 
+// The same row computed by the 32 - SPLIT fix-up lanes of the producer warp
+// together (dim <= 32 - SPLIT): lane SPLIT + f loads neighbour f, so all the
+// row's loads are in flight at once; every lane folds the row in numpy's
+// order from shuffles (the result is used by fix-up lane 0).
+template <int SPLIT>
+__device__ __noinline__ double2 hc_marked_row_coop(const HcStreamArgs& a, double g, const double2* __restrict__ tin,
+                                                   int64_t vl, int64_t vg, int fl) {
+  constexpr unsigned fm = ~((SPLIT == 32) ? 0xffffffffu : ((1u << SPLIT) - 1u));
+  double2 nb = make_double2(0.0, 0.0);
+  if (fl < a.dim)
+    nb = fl < a.dim_loc ? __ldg(tin + (vl ^ (1LL << fl))) : __ldg(a.remote[fl - a.dim_loc] + vl);
+  const double2 own = __ldg(tin + vl);
+  StreamRow sr;
+  sr.init(a.dim + 1);
+  const double2 gg = make_double2(g, 0.0);
+  auto pushb = [&](int b) {
+    const double2 e = make_double2(__shfl_sync(fm, nb.x, b + SPLIT), __shfl_sync(fm, nb.y, b + SPLIT));
+    sr.push(cmul_np(gg, e));
+  };
+  for (int b = a.dim - 1; b >= 0; --b)
+    if ((vg >> b) & 1) pushb(b);
+  sr.push(cmul_np(make_double2(-1.0, 0.0), own));
+  for (int b = 0; b < a.dim; ++b)
+    if (!((vg >> b) & 1)) pushb(b);
+  return sr.result();
+}
+
 // NS: ring stages; SPLIT: producer lanes, each copying 1/SPLIT of a chunk;
 // CONS: consumer threads (+ one producer warp), TILE / CONS vertices each
 template <int NS, int SPLIT, int CONS>
@@ -479,18 +506,38 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
     } else if (op.bits) {
       // ---------------- fix-up lanes: marked rows (length dim + 1, the
       // diagonal -psi[v] between the set and the clear neighbours) of this
-      // CTA's tiles; the consumers leave those vertices alone
+      // CTA's tiles; the consumers leave those vertices alone.  The 32 - SPLIT
+      // lanes scan the bitmap words together; per marked vertex lane f loads
+      // neighbour f (all loads in flight at once) and lane 0 of the group
+      // folds the row in numpy's order from shuffles.
+      constexpr int NF = 32 - SPLIT;
+      constexpr unsigned fm = ~((SPLIT == 32) ? 0xffffffffu : ((1u << SPLIT) - 1u));
+      const int fl = pl - SPLIT;
+      const bool coop = dim <= NF;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        for (int w = pl - SPLIT; w < TILE / 32; w += 32 - SPLIT) {
-          uint32_t word = __ldg(op.bits + ((vbase + (tile << LB)) >> 5) + w);
-          while (word) {
-            const int bit = __ffs(word) - 1;
-            word &= word - 1;
-            const int64_t v = (tile << LB) + w * 32 + bit;
-            const double2 t = cmul_np(alpha, hc_marked_row(op, g, tin, v, vbase + v));
-            tout[v] = t;
-            acc_out[v] = cadd(acc_in[v], cmul_np(one, t));
-            nrm = __fma_rn(t.x, t.x, __fma_rn(t.y, t.y, nrm));
+        for (int w0 = 0; w0 < TILE / 32; w0 += NF) {
+          const int w = w0 + fl;
+          const uint32_t word = w < TILE / 32 ? __ldg(op.bits + ((vbase + (tile << LB)) >> 5) + w) : 0u;
+          unsigned any = __ballot_sync(fm, word != 0u);
+          while (any) {
+            const int src = __ffs(any) - 1;
+            any &= any - 1;
+            uint32_t wd = __shfl_sync(fm, word, src);
+            const int ws = w0 + src - SPLIT;
+            while (wd) {
+              const int bit = __ffs(wd) - 1;
+              wd &= wd - 1;
+              const int64_t v = (tile << LB) + ws * 32 + bit;
+              const int64_t vg = vbase + v;
+              const double2 h = coop ? hc_marked_row_coop<SPLIT>(op, g, tin, v, vg, fl)
+                                     : hc_marked_row(op, g, tin, v, vg);
+              if (fl == 0) {
+                const double2 t = cmul_np(alpha, h);
+                tout[v] = t;
+                acc_out[v] = cadd(acc_in[v], cmul_np(one, t));
+                nrm = __fma_rn(t.x, t.x, __fma_rn(t.y, t.y, nrm));
+              }
+            }
           }
         }
       }

@@ -8,7 +8,8 @@ from paper_2406_08186_b200 import ctqw as CT
 
 dim = int(sys.argv[1]) if len(sys.argv) > 1 else 22
 eng = q.init_engine("b200")
-cs = q.CtqwSpec(q.graphs.hypercube(dim), 1.0 / dim, 1.0, frozenset({0}))
+marked = frozenset() if os.environ.get("C4_UNMARKED") else frozenset({0})
+cs = q.CtqwSpec(q.graphs.hypercube(dim), 1.0 / dim, 1.0, marked)
 op = CT._Operator(eng, cs)
 n = 1 << dim
 x = torch.full((n,), 1.0 / np.sqrt(n), dtype=torch.complex128, device="cuda")
