@@ -369,45 +369,23 @@ struct HcStream {
 };
 using HcStreamArgs = HcStream;
 
-// marked row v: -1 * psi[v] sits between the set and the clear neighbours
-// (row length dim + 1); out of line so the streaming loop keeps its registers.
-// vl: local index, vg: global vertex id; neighbours across rank bits come
-// from the partner shards' term buffers.
+// Marked row v (length dim + 1: -1 * psi[v] sits between the set and the
+// clear neighbours), computed by the fix-up warp together: lane f loads
+// neighbour f, so all the row's loads are in flight at once, and every lane
+// folds the row in numpy's order from shuffles (the result is used by lane 0).
+// vl: local index, vg: global vertex id; neighbours across rank bits come from
+// the partner shards' term buffers.  dim <= 32.
 __device__ __noinline__ double2 hc_marked_row(const HcStreamArgs& a, double g, const double2* __restrict__ tin,
-                                              int64_t vl, int64_t vg) {
-  auto fetch = [&](int b) {
-    return b < a.dim_loc ? __ldg(tin + (vl ^ (1LL << b))) : __ldg(a.remote[b - a.dim_loc] + vl);
-  };
-  StreamRow sr;
-  sr.init(a.dim + 1);
-  const double2 gg = make_double2(g, 0.0);
-  for (int b = a.dim - 1; b >= 0; --b)
-    if ((vg >> b) & 1) sr.push(cmul_np(gg, fetch(b)));
-  sr.push(cmul_np(make_double2(-1.0, 0.0), __ldg(tin + vl)));
-  for (int b = 0; b < a.dim; ++b)
-    if (!((vg >> b) & 1)) sr.push(cmul_np(gg, fetch(b)));
-  return sr.result();
-}
-
-
-
-// The same row computed by the 32 - SPLIT fix-up lanes of the producer warp
-// together (dim <= 32 - SPLIT): lane SPLIT + f loads neighbour f, so all the
-// row's loads are in flight at once; every lane folds the row in numpy's
-// order from shuffles (the result is used by fix-up lane 0).
-template <int SPLIT>
-__device__ __noinline__ double2 hc_marked_row_coop(const HcStreamArgs& a, double g, const double2* __restrict__ tin,
-                                                   int64_t vl, int64_t vg, int fl) {
-  constexpr unsigned fm = ~((SPLIT == 32) ? 0xffffffffu : ((1u << SPLIT) - 1u));
+                                              int64_t vl, int64_t vg, int lane) {
   double2 nb = make_double2(0.0, 0.0);
-  if (fl < a.dim)
-    nb = fl < a.dim_loc ? __ldg(tin + (vl ^ (1LL << fl))) : __ldg(a.remote[fl - a.dim_loc] + vl);
+  if (lane < a.dim)
+    nb = lane < a.dim_loc ? __ldg(tin + (vl ^ (1LL << lane))) : __ldg(a.remote[lane - a.dim_loc] + vl);
   const double2 own = __ldg(tin + vl);
   StreamRow sr;
   sr.init(a.dim + 1);
   const double2 gg = make_double2(g, 0.0);
   auto pushb = [&](int b) {
-    const double2 e = make_double2(__shfl_sync(fm, nb.x, b + SPLIT), __shfl_sync(fm, nb.y, b + SPLIT));
+    const double2 e = make_double2(__shfl_sync(0xffffffffu, nb.x, b), __shfl_sync(0xffffffffu, nb.y, b));
     sr.push(cmul_np(gg, e));
   };
   for (int b = a.dim - 1; b >= 0; --b)
@@ -419,9 +397,10 @@ __device__ __noinline__ double2 hc_marked_row_coop(const HcStreamArgs& a, double
 }
 
 // NS: ring stages; SPLIT: producer lanes, each copying 1/SPLIT of a chunk;
-// CONS: consumer threads (+ one producer warp), TILE / CONS vertices each
+// CONS: consumer threads (+ one producer warp + one fix-up warp), TILE / CONS
+// vertices each
 template <int NS, int SPLIT, int CONS>
-__global__ void __launch_bounds__(CONS + 32, 1)
+__global__ void __launch_bounds__(CONS + 64, 1)
 hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* __restrict__ tin, double2* __restrict__ tout,
                  const double2* acc_in, double2* acc_out, double s_k, const int* __restrict__ done,
                  double* __restrict__ partial) {
@@ -435,7 +414,7 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
   uint64_t* empty = full + NS;
   uint64_t* afull = empty + NS;                                // [2]
   uint64_t* aempty = afull + 2;                                // [2]
-  __shared__ double red[CONS / 32 + 1];
+  __shared__ double red[CONS / 32 + 2];
   const int tid = threadIdx.x;
   const int dim = op.dim;
   const int nh = dim - LB;                            // high bits (global)
@@ -465,7 +444,7 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
 
   if (tid >= CONS) {
     const int pl = tid - CONS;
-    if (pl < SPLIT) {
+    if (pl < SPLIT) {   // (lanes SPLIT..31 of the producer warp idle)
       // ---------------- producer lanes: stream the partner tiles in row order
       constexpr unsigned pmask = (SPLIT == 32) ? 0xffffffffu : ((1u << SPLIT) - 1u);
       constexpr uint32_t part = CHUNK_BYTES / SPLIT;
@@ -503,40 +482,30 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
           ++it;
         }
       }
-    } else if (op.bits) {
-      // ---------------- fix-up lanes: marked rows (length dim + 1, the
-      // diagonal -psi[v] between the set and the clear neighbours) of this
-      // CTA's tiles; the consumers leave those vertices alone.  The 32 - SPLIT
-      // lanes scan the bitmap words together; per marked vertex lane f loads
-      // neighbour f (all loads in flight at once) and lane 0 of the group
-      // folds the row in numpy's order from shuffles.
-      constexpr int NF = 32 - SPLIT;
-      constexpr unsigned fm = ~((SPLIT == 32) ? 0xffffffffu : ((1u << SPLIT) - 1u));
-      const int fl = pl - SPLIT;
-      const bool coop = dim <= NF;
+    } else if (pl >= 32 && op.bits) {
+      // ---------------- fix-up warp: marked rows of this CTA's tiles (the
+      // consumers leave those vertices alone).  Its own warp: sharing the
+      // producer's warp, the bitmap scan held up the stream (+15 us/term).
+      // The lanes scan the bitmap words together; per marked vertex the warp
+      // computes the row cooperatively and lane 0 stores it.
+      const int fl = pl - 32;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        for (int w0 = 0; w0 < TILE / 32; w0 += NF) {
-          const int w = w0 + fl;
-          const uint32_t word = w < TILE / 32 ? __ldg(op.bits + ((vbase + (tile << LB)) >> 5) + w) : 0u;
-          unsigned any = __ballot_sync(fm, word != 0u);
-          while (any) {
-            const int src = __ffs(any) - 1;
-            any &= any - 1;
-            uint32_t wd = __shfl_sync(fm, word, src);
-            const int ws = w0 + src - SPLIT;
-            while (wd) {
-              const int bit = __ffs(wd) - 1;
-              wd &= wd - 1;
-              const int64_t v = (tile << LB) + ws * 32 + bit;
-              const int64_t vg = vbase + v;
-              const double2 h = coop ? hc_marked_row_coop<SPLIT>(op, g, tin, v, vg, fl)
-                                     : hc_marked_row(op, g, tin, v, vg);
-              if (fl == 0) {
-                const double2 t = cmul_np(alpha, h);
-                tout[v] = t;
-                acc_out[v] = cadd(acc_in[v], cmul_np(one, t));
-                nrm = __fma_rn(t.x, t.x, __fma_rn(t.y, t.y, nrm));
-              }
+        const uint32_t word = __ldg(op.bits + ((vbase + (tile << LB)) >> 5) + fl);   // TILE / 32 == 32 words
+        unsigned any = __ballot_sync(0xffffffffu, word != 0u);
+        while (any) {
+          const int src = __ffs(any) - 1;
+          any &= any - 1;
+          uint32_t wd = __shfl_sync(0xffffffffu, word, src);
+          while (wd) {
+            const int bit = __ffs(wd) - 1;
+            wd &= wd - 1;
+            const int64_t v = (tile << LB) + src * 32 + bit;
+            const double2 h = hc_marked_row(op, g, tin, v, vbase + v, fl);
+            if (fl == 0) {
+              const double2 t = cmul_np(alpha, h);
+              tout[v] = t;
+              acc_out[v] = cadd(acc_in[v], cmul_np(one, t));
+              nrm = __fma_rn(t.x, t.x, __fma_rn(t.y, t.y, nrm));
             }
           }
         }
@@ -621,7 +590,10 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
 #pragma unroll
       for (int j = 0; j < VPT; ++j) {
         const int64_t v = ((int64_t)H << LB) + tid + j * CONS;   // global id
-        mword[j] = op.bits ? __ldg(op.bits + (v >> 5)) : 0u;
+        // asm volatile keeps the load here, ahead of the stream's waits (the
+        // compiler otherwise sinks it to the epilogue and exposes its latency)
+        mword[j] = 0u;
+        if (op.bits) asm volatile("ld.global.nc.u32 %0, [%1];\n" : "=r"(mword[j]) : "l"(op.bits + (v >> 5)));
       }
       // one stage: wait for it, read and scale this thread's entries, release
       auto take = [&](double2 (&e)[VPT]) {
@@ -733,7 +705,7 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
   __syncthreads();
   if (tid == 0) {
     double r = 0.0;
-    for (int w = 0; w < CONS / 32 + 1; ++w) r = __dadd_rn(r, red[w]);
+    for (int w = 0; w < CONS / 32 + 2; ++w) r = __dadd_rn(r, red[w]);
     partial[blockIdx.x] = r;
   }
 }
@@ -749,7 +721,7 @@ void launch_stream(const HcStream& op, cudaStream_t s, int64_t n, const double2*
                          (int)hcs::smem_bytes(NS));
     configured[dev] = true;
   }
-  hc_stream_kernel<NS, SPLIT, CONS><<<op.grid, CONS + 32, hcs::smem_bytes(NS), s>>>(op, n, tin, tout, ain, acc,
+  hc_stream_kernel<NS, SPLIT, CONS><<<op.grid, CONS + 64, hcs::smem_bytes(NS), s>>>(op, n, tin, tout, ain, acc,
                                                                                     s_k, flags, partial);
 }
 
