@@ -729,14 +729,16 @@ int launch_term(const HcStream& op, cudaStream_t s, int64_t n, const double2* ti
                 const double2* ain, double2* acc, double s_k, const int* flags, double* partial) {
   // QWB_HC_STREAM = CONS/256 * 10000 + NS * 100 + SPLIT (tuning knob; measured at
   // dim 22: 601 173, 20601 157, 20801 143-144.5, 21001 139.6, 21201 140.7,
-  // 20804 166 us/term)
+  // 20804 166 us/term; with the separate fix-up warp: 11001 141.7, 20801
+  // 117.6, 21001 111.4-111.7, 21201 109.8-110.5)
   switch (op.variant) {
     case 601: launch_stream<6, 1, 256>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
     case 20601: launch_stream<6, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
-    case 21201: launch_stream<12, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+    case 11001: launch_stream<10, 1, 256>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+    case 21001: launch_stream<10, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
     case 20804: launch_stream<8, 4, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
     case 20801: launch_stream<8, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
-    default: launch_stream<10, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+    default: launch_stream<12, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
   }
   return op.grid;
 }
@@ -959,7 +961,7 @@ int hc_stream_base(qwb_ctx* ctx, int dim, int S, double gamma, const uint32_t* b
   static int variant = -1;
   if (variant < 0) {
     const char* e = getenv("QWB_HC_STREAM");
-    variant = (e && *e) ? atoi(e) : 21001;
+    variant = (e && *e) ? atoi(e) : 21201;
   }
   const int64_t ntiles = 1LL << (dim - S - hcs::LB);
   *op = HcStream{};
