@@ -415,6 +415,7 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
   uint64_t* afull = empty + NS;                                // [2]
   uint64_t* aempty = afull + 2;                                // [2]
   __shared__ double red[CONS / 32 + 2];
+  __shared__ uint32_t mwords[CONS / 32][TILE / CONS];   // consumers: the tile's bitmap words
   const int tid = threadIdx.x;
   const int dim = op.dim;
   const int nh = dim - LB;                            // high bits (global)
@@ -585,15 +586,19 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
           }
         }
       };
-      // the marked-bitmap words are loaded now and land while the stream is folded
-      uint32_t mword[VPT];
+      // the tile's marked-bitmap words (one per warp and j: a warp's 32
+      // vertices share a word) are copied to shared memory by lane 0 with
+      // cp.async now and land while the stream is folded (a register load
+      // here was spilled, and the spill store waited for the load)
+      if (op.bits && lane == 0) {
 #pragma unroll
-      for (int j = 0; j < VPT; ++j) {
-        const int64_t v = ((int64_t)H << LB) + tid + j * CONS;   // global id
-        // asm volatile keeps the load here, ahead of the stream's waits (the
-        // compiler otherwise sinks it to the epilogue and exposes its latency)
-        mword[j] = 0u;
-        if (op.bits) asm volatile("ld.global.nc.u32 %0, [%1];\n" : "=r"(mword[j]) : "l"(op.bits + (v >> 5)));
+        for (int j = 0; j < VPT; ++j) {
+          const int64_t v = ((int64_t)H << LB) + tid + j * CONS;   // global id
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(&mwords[tid >> 5][j])),
+                       "l"(op.bits + (v >> 5))
+                       : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
       }
       // one stage: wait for it, read and scale this thread's entries, release
       auto take = [&](double2 (&e)[VPT]) {
@@ -684,10 +689,15 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
       const int ab = ti & 1;
       mbar_wait(afull + ab, (ti >> 1) & 1);
       const double2* ach = accbuf + (size_t)ab * TILE;
+      if (op.bits) {
+        if (lane == 0) asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncwarp();
+      }
 #pragma unroll
       for (int j = 0; j < VPT; ++j) {
         const int64_t v = (tile << LB) + tid + j * CONS;            // local index
-        if ((mword[j] >> (v & 31)) & 1u) continue;   // marked: fix-up lanes
+        const uint32_t mword = op.bits ? mwords[tid >> 5][j] : 0u;
+        if ((mword >> (v & 31)) & 1u) continue;   // marked: the fix-up warp's
         const double2 r = (m == main_end) ? cadd(cadd(ac[0][j], ac[1][j]), cadd(ac[2][j], ac[3][j])) : ac[0][j];
         const double2 t = cmul_np(alpha, cadd(x0[j], r));
         tout[v] = t;
