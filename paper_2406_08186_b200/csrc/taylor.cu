@@ -296,6 +296,11 @@ constexpr uint32_t CHUNK_BYTES = TILE * sizeof(double2);
 constexpr size_t smem_bytes(int ns) { return (size_t)(ns + 2) * CHUNK_BYTES + (2 * ns + 4) * sizeof(uint64_t); }
 }  // namespace hcs
 
+__device__ __forceinline__ uint32_t nctaid_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nctaid.x;" : "=r"(r));
+  return r;
+}
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -549,7 +554,9 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
     // partners in one of four compile-time rotations).
     const uint32_t full_u32 = smem_u32(full), empty_u32 = smem_u32(empty);
     uint32_t s = 0, ph = 0, ti = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
+    // 32-bit tile index, stride re-read from %nctaid (a 64-bit index and a
+    // hoisted stride were spilled; the reload missed the small L1)
+    for (uint32_t tile = blockIdx.x; tile < (uint32_t)ntiles; tile += nctaid_x(), ++ti) {
       const uint32_t H = hbase | (uint32_t)tile;   // global tile index: row order
       const int hs = __popc(H);
       double2 x0[VPT], ac[4][VPT];
@@ -695,7 +702,7 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
       }
 #pragma unroll
       for (int j = 0; j < VPT; ++j) {
-        const int64_t v = (tile << LB) + tid + j * CONS;            // local index
+        const int64_t v = ((int64_t)tile << LB) + tid + j * CONS;   // local index
         const uint32_t mword = op.bits ? mwords[tid >> 5][j] : 0u;
         if ((mword >> (v & 31)) & 1u) continue;   // marked: the fix-up warp's
         const double2 r = (m == main_end) ? cadd(cadd(ac[0][j], ac[1][j]), cadd(ac[2][j], ac[3][j])) : ac[0][j];
