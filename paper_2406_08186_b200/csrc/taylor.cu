@@ -33,6 +33,7 @@ using qwb::cmul_np;
 
 constexpr int kTermBlocks = 2048;   // fixed grid => deterministic partial order
 constexpr int kTermThreads = 256;
+constexpr int kPartialsMax = 16384;  // partial-sum slots in the evolve workspace
 
 // Streaming x0 + pairwise(x1..x{L-1}) for rows of L <= 65 entries, element by
 // element in order (numpy block rule with four rotating complex accumulators).
@@ -71,6 +72,7 @@ struct CsrOp {
   const int64_t* __restrict__ offs;
   const int32_t* __restrict__ col;
   const double2* __restrict__ val;
+  int grid;   // term-kernel blocks: one resident wave (set by qwb_taylor_evolve_csr)
   struct Get {
     const int32_t* __restrict__ col;
     const double2* __restrict__ val;
@@ -82,7 +84,35 @@ struct CsrOp {
     }
   };
   __device__ __forceinline__ double2 row(int64_t v, const double2* __restrict__ x) const {
-    const int64_t s = offs[v], e = offs[v + 1];
+    const int64_t s = __ldg(offs + v), e = __ldg(offs + v + 1);
+    const int64_t len = e - s;
+    if (len == 4 || len == 5) {
+      // short rows (every row of a lattice / cycle H, marked rows one longer):
+      // all column, value and neighbour loads issued up front, then numpy's
+      // x0 + pairwise(x1..): sequential from -0 for 3 rest elements, the
+      // (c0+c1)+(c2+c3) block for 4
+      int c[5];
+      double2 w[5], xv[5];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) c[i] = __ldg(col + s + i);
+      c[4] = (len == 5) ? __ldg(col + s + 4) : c[3];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) w[i] = __ldg(val + s + i);
+      w[4] = (len == 5) ? __ldg(val + s + 4) : w[3];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) xv[i] = __ldg(x + c[i]);
+      xv[4] = (len == 5) ? __ldg(x + c[4]) : xv[3];
+      double2 p[5];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) p[i] = cmul_np(w[i], xv[i]);
+      double2 r;
+      if (len == 4) {
+        r = cadd(cadd(cadd(make_double2(-0.0, -0.0), p[1]), p[2]), p[3]);
+      } else {
+        r = cadd(cadd(p[1], p[2]), cadd(p[3], p[4]));
+      }
+      return cadd(p[0], r);
+    }
     if (e == s) return make_double2(0.0, 0.0);
     Get g{col, val, x, s};
     return qwb::reduceat_z(g, e - s);
@@ -774,6 +804,16 @@ int launch_term(const Op& op, cudaStream_t s, int64_t n, const double2* tin, dou
   return kTermBlocks;
 }
 
+// CSR term: a grid of exactly one resident wave (SMs x resident CTAs) — the
+// grid-stride loop then has no partial last wave (2048 blocks were 4.6 waves:
+// 140 -> 126 us/term on a 2048^2 grid H).  Deterministic for a given device.
+int launch_term(const CsrOp& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
+                const double2* ain, double2* acc, double s_k, const int* flags, double* partial) {
+  const int grid = op.grid;
+  term_kernel<CsrOp><<<grid, kTermThreads, 0, s>>>(op, n, tin, tout, ain, acc, s_k, flags, partial);
+  return grid;
+}
+
 
 __global__ void apply_kernel_hc(HypercubeOp<32> op, int64_t n, const double2* __restrict__ x,
                                 double2* __restrict__ y) {
@@ -788,10 +828,10 @@ int evolve(qwb_ctx* ctx, const Op& op, int64_t n, double2* psi, double2* work, i
   if (substeps < 1) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "substeps must be >= 1");
   if (max_terms < 1) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "max_terms must be >= 1");
   void* ws;
-  int st = qwb::workspace(ctx, kTermBlocks * sizeof(double) + 256, s, &ws);
+  int st = qwb::workspace(ctx, kPartialsMax * sizeof(double) + 256, s, &ws);
   if (st) return st;
   double* partial = reinterpret_cast<double*>(ws);
-  int* flags = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + kTermBlocks * sizeof(double));
+  int* flags = reinterpret_cast<int*>(reinterpret_cast<char*>(ws) + kPartialsMax * sizeof(double));
   int* pin = reinterpret_cast<int*>(ctx->pinned);
   // 4 distinct buffers: cur, acc, term ping-pong
   double2* bufs[4] = {psi, work, work + n, work + 2 * n};
@@ -1046,7 +1086,12 @@ int qwb_taylor_evolve_csr(qwb_ctx* ctx, int64_t n, const int64_t* row_offsets, c
                           double floor, int max_terms, int* terms_host, void* stream) {
   QWB_BEGIN(ctx);
   if (n < 1) QWB_FAIL(ctx, QWB_E_DIMENSION, "dimension must be positive");
-  CsrOp op{row_offsets, col, reinterpret_cast<const double2*>(val)};
+  int per_sm = 0;
+  QWB_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, term_kernel<CsrOp>,
+                                                              kTermThreads, 0));
+  int grid = (per_sm > 0 ? per_sm : 1) * ctx->num_sms;
+  if (grid > kPartialsMax) grid = kPartialsMax;
+  CsrOp op{row_offsets, col, reinterpret_cast<const double2*>(val), grid};
   return evolve(ctx, op, n, reinterpret_cast<double2*>(psi), reinterpret_cast<double2*>(work),
                 substeps, tau, floor, max_terms, terms_host, qwb::as_stream(stream));
 }
