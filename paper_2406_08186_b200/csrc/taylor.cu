@@ -72,7 +72,8 @@ struct CsrOp {
   const int64_t* __restrict__ offs;
   const int32_t* __restrict__ col;
   const double2* __restrict__ val;
-  int grid;   // term-kernel blocks: one resident wave (set by qwb_taylor_evolve_csr)
+  int grid;     // term-kernel blocks: one resident wave (set by qwb_taylor_evolve_csr)
+  int capped;   // 1: csr_term_kernel4 (64 registers), 0: term_kernel<CsrOp>
   struct Get {
     const int32_t* __restrict__ col;
     const double2* __restrict__ val;
@@ -114,8 +115,13 @@ struct CsrOp {
       return cadd(p[0], r);
     }
     if (e == s) return make_double2(0.0, 0.0);
+    return row_long(s, e - s, x);
+  }
+  // other lengths out of line: the generic pairwise reducer's stack stays out
+  // of the short-row path's register allocation
+  __device__ __noinline__ double2 row_long(int64_t s, int64_t len, const double2* __restrict__ x) const {
     Get g{col, val, x, s};
-    return qwb::reduceat_z(g, e - s);
+    return qwb::reduceat_z(g, len);
   }
 };
 
@@ -145,11 +151,9 @@ struct HypercubeOp {
 };
 
 template <class Op>
-__global__ void __launch_bounds__(kTermThreads)
-term_kernel(Op op, int64_t n, const double2* __restrict__ tin, double2* __restrict__ tout,
-            const double2* acc_in, double2* acc_out, double s_k, const int* __restrict__ done,
-            double* __restrict__ partial) {
-  if (*done) return;
+__device__ __forceinline__ void term_body(const Op& op, int64_t n, const double2* __restrict__ tin,
+                                          double2* __restrict__ tout, const double2* acc_in,
+                                          double2* acc_out, double s_k, double* __restrict__ partial) {
   __shared__ double sh[kTermThreads];
   const double2 alpha = make_double2(0.0, -s_k);      // Python complex(-1j * tau / k)
   const double2 one = make_double2(1.0, 0.0);
@@ -169,6 +173,27 @@ term_kernel(Op op, int64_t n, const double2* __restrict__ tin, double2* __restri
     __syncthreads();
   }
   if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+template <class Op>
+__global__ void __launch_bounds__(kTermThreads)
+term_kernel(Op op, int64_t n, const double2* __restrict__ tin, double2* __restrict__ tout,
+            const double2* acc_in, double2* acc_out, double s_k, const int* __restrict__ done,
+            double* __restrict__ partial) {
+  if (*done) return;
+  term_body(op, n, tin, tout, acc_in, acc_out, s_k, partial);
+}
+
+// CSR H: capped at 64 registers (4 resident CTAs per SM; a few spilled bytes,
+// outside the short-row loads) — the default.  QWB_CSR_TERM_MINB=3 selects the
+// uncapped term_kernel<CsrOp> (78 registers, 3 CTAs).  2048^2 grid H:
+// 126.1 -> 119.9 us/term; 4096^2: 455.5 -> 424.7 us/term (6.0 TB/s)
+__global__ void __launch_bounds__(kTermThreads, 4)
+csr_term_kernel4(CsrOp op, int64_t n, const double2* __restrict__ tin, double2* __restrict__ tout,
+                 const double2* acc_in, double2* acc_out, double s_k, const int* __restrict__ done,
+                 double* __restrict__ partial) {
+  if (*done) return;
+  term_body(op, n, tin, tout, acc_in, acc_out, s_k, partial);
 }
 
 __global__ void __launch_bounds__(kTermThreads)
@@ -810,7 +835,10 @@ int launch_term(const Op& op, cudaStream_t s, int64_t n, const double2* tin, dou
 int launch_term(const CsrOp& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
                 const double2* ain, double2* acc, double s_k, const int* flags, double* partial) {
   const int grid = op.grid;
-  term_kernel<CsrOp><<<grid, kTermThreads, 0, s>>>(op, n, tin, tout, ain, acc, s_k, flags, partial);
+  if (op.capped)
+    csr_term_kernel4<<<grid, kTermThreads, 0, s>>>(op, n, tin, tout, ain, acc, s_k, flags, partial);
+  else
+    term_kernel<CsrOp><<<grid, kTermThreads, 0, s>>>(op, n, tin, tout, ain, acc, s_k, flags, partial);
   return grid;
 }
 
@@ -1086,12 +1114,21 @@ int qwb_taylor_evolve_csr(qwb_ctx* ctx, int64_t n, const int64_t* row_offsets, c
                           double floor, int max_terms, int* terms_host, void* stream) {
   QWB_BEGIN(ctx);
   if (n < 1) QWB_FAIL(ctx, QWB_E_DIMENSION, "dimension must be positive");
+  static int capped = -1;
+  if (capped < 0) {
+    const char* e = getenv("QWB_CSR_TERM_MINB");
+    capped = (e && *e && atoi(e) == 3) ? 0 : 1;   // default: the 4-CTA kernel
+  }
   int per_sm = 0;
-  QWB_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, term_kernel<CsrOp>,
-                                                              kTermThreads, 0));
+  if (capped)
+    QWB_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_term_kernel4,
+                                                                kTermThreads, 0));
+  else
+    QWB_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, term_kernel<CsrOp>,
+                                                                kTermThreads, 0));
   int grid = (per_sm > 0 ? per_sm : 1) * ctx->num_sms;
   if (grid > kPartialsMax) grid = kPartialsMax;
-  CsrOp op{row_offsets, col, reinterpret_cast<const double2*>(val), grid};
+  CsrOp op{row_offsets, col, reinterpret_cast<const double2*>(val), grid, capped};
   return evolve(ctx, op, n, reinterpret_cast<double2*>(psi), reinterpret_cast<double2*>(work),
                 substeps, tau, floor, max_terms, terms_host, qwb::as_stream(stream));
 }
