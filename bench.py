@@ -665,6 +665,32 @@ def measure_extras(q, CO, eng, dev, peak):
                                           "per vertex-term over L2->SM): the term is L2-bandwidth and "
                                           "latency bound, not HBM bound",
                                   "inf_norm": op.inf_norm}
+    del op, x
+    torch.cuda.empty_cache()
+
+    # CTQW on a generic (CSR) H: grid 2048^2, gamma 0.25, marked {0}, t = 1
+    nx = 2048
+    csp = q.CtqwSpec(q.graphs.grid(nx, nx), 0.25, 1.0, frozenset({0}))
+    opc = CT._Operator(eng, csp)
+    nv = nx * nx
+    xc = torch.full((nv,), 1.0 / np.sqrt(nv), dtype=torch.complex128, device=dev)
+    opc.evolve(xc, 1.0, 1e-12)
+    xc.fill_(1.0 / np.sqrt(nv))
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    terms = opc.evolve(xc, 1.0, 1e-12)
+    torch.cuda.synchronize(dev)
+    dt = time.perf_counter() - t0
+    nterms = sum(terms)
+    per_vt = 64 + 20 * (4 * nv + 1) / nv + 8   # state r/w + acc RMW, values + cols, row offsets
+    out["ctqw_csr_grid2048"] = {"terms": terms, "us_per_term": dt / nterms * 1e6,
+                                "vertex_term_updates_per_s": nv * nterms / dt,
+                                "bytes_per_vertex_term": per_vt,
+                                "achieved_GBps": per_vt * nv * nterms / dt / 1e9,
+                                "frac": per_vt * nv * nterms / dt / 1e9 / peak,
+                                "kernel": "csr_term_kernel4 (one resident wave, 64 registers)",
+                                "note": "wall time of one evolve (incl. the per-term norm finalize and "
+                                        "the per-chunk stop-flag reads)"}
     return out
 
 
