@@ -23,6 +23,7 @@
 // order, v with its set bits cleared high->low, the diagonal (if v marked),
 // then v with its clear bits set low->high.
 #include <type_traits>
+#include <utility>
 
 #include "qwb_internal.cuh"
 
@@ -34,6 +35,35 @@ using qwb::cmul_np;
 constexpr int kTermBlocks = 2048;   // fixed grid => deterministic partial order
 constexpr int kTermThreads = 256;
 constexpr int kPartialsMax = 16384;  // partial-sum slots in the evolve workspace
+
+// Programmatic dependent launch (PDL) around the term chain: wait until the
+// previous kernel in the stream has completed and its writes are visible (the
+// `done` flag included), then let the next one be scheduled so its launch
+// latency hides behind this kernel.  Both are no-ops without the attribute.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
+// launch with the PDL attribute (QWB_TERM_PDL=0 turns it off)
+template <class... P, class... A>
+cudaError_t launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... args) {
+  static int pdl = [] {
+    const char* e = getenv("QWB_TERM_PDL");
+    return (e && *e) ? atoi(e) : 1;
+  }();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
+}
 
 // Streaming x0 + pairwise(x1..x{L-1}) for rows of L <= 65 entries, element by
 // element in order (numpy block rule with four rotating complex accumulators).
@@ -180,6 +210,7 @@ __global__ void __launch_bounds__(kTermThreads)
 term_kernel(Op op, int64_t n, const double2* __restrict__ tin, double2* __restrict__ tout,
             const double2* acc_in, double2* acc_out, double s_k, const int* __restrict__ done,
             double* __restrict__ partial) {
+  pdl_enter();
   if (*done) return;
   term_body(op, n, tin, tout, acc_in, acc_out, s_k, partial);
 }
@@ -192,6 +223,7 @@ __global__ void __launch_bounds__(kTermThreads, 4)
 csr_term_kernel4(CsrOp op, int64_t n, const double2* __restrict__ tin, double2* __restrict__ tout,
                  const double2* acc_in, double2* acc_out, double s_k, const int* __restrict__ done,
                  double* __restrict__ partial) {
+  pdl_enter();
   if (*done) return;
   term_body(op, n, tin, tout, acc_in, acc_out, s_k, partial);
 }
@@ -199,6 +231,7 @@ csr_term_kernel4(CsrOp op, int64_t n, const double2* __restrict__ tin, double2* 
 __global__ void __launch_bounds__(kTermThreads)
 term_finalize_kernel(const double* __restrict__ partial, int nparts, double floor_, int k,
                      int* __restrict__ done, int* __restrict__ terms) {
+  pdl_enter();
   if (*done) return;
   __shared__ double sh[kTermThreads];
   double acc = 0.0;
@@ -466,6 +499,7 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
                  double* __restrict__ partial) {
   using namespace hcs;
   constexpr int VPT = TILE / CONS;
+  pdl_enter();
   if (*done) return;
   extern __shared__ __align__(128) unsigned char hcs_smem[];
   double2* ring = reinterpret_cast<double2*>(hcs_smem);
@@ -793,8 +827,8 @@ void launch_stream(const HcStream& op, cudaStream_t s, int64_t n, const double2*
                          (int)hcs::smem_bytes(NS));
     configured[dev] = true;
   }
-  hc_stream_kernel<NS, SPLIT, CONS><<<op.grid, CONS + 64, hcs::smem_bytes(NS), s>>>(op, n, tin, tout, ain, acc,
-                                                                                    s_k, flags, partial);
+  launch_pdl(hc_stream_kernel<NS, SPLIT, CONS>, op.grid, CONS + 64, hcs::smem_bytes(NS), s, op, n, tin, tout,
+             ain, acc, s_k, flags, partial);
 }
 
 int launch_term(const HcStream& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
@@ -836,9 +870,9 @@ int launch_term(const CsrOp& op, cudaStream_t s, int64_t n, const double2* tin, 
                 const double2* ain, double2* acc, double s_k, const int* flags, double* partial) {
   const int grid = op.grid;
   if (op.capped)
-    csr_term_kernel4<<<grid, kTermThreads, 0, s>>>(op, n, tin, tout, ain, acc, s_k, flags, partial);
+    launch_pdl(csr_term_kernel4, grid, kTermThreads, 0, s, op, n, tin, tout, ain, acc, s_k, flags, partial);
   else
-    term_kernel<CsrOp><<<grid, kTermThreads, 0, s>>>(op, n, tin, tout, ain, acc, s_k, flags, partial);
+    launch_pdl(term_kernel<CsrOp>, grid, kTermThreads, 0, s, op, n, tin, tout, ain, acc, s_k, flags, partial);
   return grid;
 }
 
@@ -888,8 +922,8 @@ int evolve(qwb_ctx* ctx, const Op& op, int64_t n, double2* psi, double2* work, i
         const double2* ain = (k == 1) ? bufs[cur] : acc;
         const double s_k = tau / (double)k;
         const int nparts = launch_term(op, s, n, tin, tout, ain, acc, s_k, flags, partial);
-        term_finalize_kernel<<<1, kTermThreads, 0, s>>>(partial, nparts, floor_, k, flags,
-                                                        flags + 1);
+        launch_pdl(term_finalize_kernel, 1, kTermThreads, 0, s, (const double*)partial, nparts, floor_, k,
+                   flags, flags + 1);
       }
       QWB_LAUNCH_CHECK(ctx, "term kernels");
       launched = upto;
