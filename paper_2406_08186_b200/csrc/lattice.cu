@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(256)
 lattice_step_kernel(Geom g, Rows rows, const double2* __restrict__ in, double2* __restrict__ out,
                     const uint32_t* __restrict__ bits, double* __restrict__ prob, int prob_row0,
                     TraceArgs tr) {
+  qwb::pdl_enter();   // the previous step's output is this step's input
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= g.nx) return;
   const int64_t P = g.pstride;
@@ -187,8 +188,9 @@ dim3 grid_for(int nx, int nrows) {
 template <int SHIFT, bool MARKED, bool PROB, bool TRACE>
 void launch_t(cudaStream_t s, const Geom& g, const Rows& r, const double2* in, double2* out,
               const uint32_t* bits, double* prob, int prob_row0, const TraceArgs& tr) {
-  lattice_step_kernel<SHIFT, MARKED, PROB, TRACE><<<grid_for(g.nx, r.nrows), 256, 0, s>>>(
-      g, r, in, out, bits, prob, prob_row0, tr);
+  static const bool pdl = qwb::env_flag("QWB_STEP_PDL", 1) != 0;   // see qwb::launch_pdl
+  qwb::launch_pdl(pdl, lattice_step_kernel<SHIFT, MARKED, PROB, TRACE>, grid_for(g.nx, r.nrows), 256, 0, s,
+                  g, r, in, out, bits, prob, prob_row0, tr);
 }
 
 template <int SHIFT>

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
+#include <utility>
 #include <string>
 
 #include "../../include/qwb200.h"
@@ -41,6 +43,43 @@ int nccl_sendrecv_list(qwb_ctx* ctx, const void* const* send, const size_t* send
                        const size_t* recv_count, const int* peers, int npeers, cudaStream_t s);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Programmatic dependent launch (PDL).  A kernel calls pdl_enter() before its
+// first global read: it waits until the previous kernel in the stream has
+// completed and its writes are visible, then lets the next kernel be scheduled
+// so that kernel's launch latency hides behind this one.  Both instructions
+// are no-ops for a launch without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+__device__ __forceinline__ void pdl_enter() {
+  pdl_wait();
+  pdl_trigger();
+}
+
+// integer environment switch (unset or empty: dflt)
+inline int env_flag(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return (e && *e) ? atoi(e) : dflt;
+}
+
+// launch `kernel` on `s`, with the PDL attribute when `pdl`
+template <class... P, class... A>
+cudaError_t launch_pdl(bool pdl, void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       A&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
+}
 
 inline unsigned blocks_for(int64_t n, int threads, int64_t cap = 1 << 30) {
   int64_t b = (n + threads - 1) / threads;

@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(256)
 spmv_kernel(int64_t n_rows, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
             const double2* __restrict__ val, const double2* __restrict__ x,
             double2* __restrict__ y) {
+  qwb::pdl_enter();   // x is the previous launch's y in the step loop
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = __ldg(rowptr + r), e = __ldg(rowptr + r + 1);
@@ -190,11 +191,10 @@ int qwb_spmv(qwb_ctx* ctx, int64_t n_rows, const int64_t* row_offsets, const int
              const qwb_z* val, const qwb_z* x, qwb_z* y, void* stream) {
   QWB_BEGIN(ctx);
   if (n_rows < 1) QWB_FAIL(ctx, QWB_E_DIMENSION, "n_rows must be positive");
-  spmv_kernel<<<qwb::blocks_for(n_rows, 256, (int64_t)ctx->num_sms * 64), 256, 0,
-                qwb::as_stream(stream)>>>(n_rows, row_offsets, col,
-                                          reinterpret_cast<const double2*>(val),
-                                          reinterpret_cast<const double2*>(x),
-                                          reinterpret_cast<double2*>(y));
+  static const bool pdl = qwb::env_flag("QWB_STEP_PDL", 1) != 0;   // see qwb::launch_pdl
+  qwb::launch_pdl(pdl, spmv_kernel, qwb::blocks_for(n_rows, 256, (int64_t)ctx->num_sms * 64), 256, 0,
+                  qwb::as_stream(stream), n_rows, row_offsets, col, reinterpret_cast<const double2*>(val),
+                  reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y));
   QWB_LAUNCH_CHECK(ctx, "spmv_kernel");
   return QWB_OK;
 }
@@ -234,10 +234,12 @@ int qwb_csr_run(qwb_ctx* ctx, int64_t n_rows, const int64_t* row_offsets, const 
   double2* b = a + n_rows;
   QWB_CUDA(ctx, cudaMemcpyAsync(a, psi0, n_rows * sizeof(double2), cudaMemcpyDeviceToDevice, s));
   const unsigned grid = qwb::blocks_for(n_rows, 256, (int64_t)ctx->num_sms * 64);
+  static const bool pdl = qwb::env_flag("QWB_STEP_PDL", 1) != 0;   // see qwb::launch_pdl
   int64_t cur = 0;
   for (int64_t j = 0; j < n_snap; ++j) {
     for (; cur < k_host[j]; ++cur) {
-      spmv_kernel<<<grid, 256, 0, s>>>(n_rows, row_offsets, col, v, a, b);
+      qwb::launch_pdl(pdl, spmv_kernel, grid, 256, 0, s, n_rows, row_offsets, col, v,
+                      (const double2*)a, b);
       double2* t = a;
       a = b;
       b = t;

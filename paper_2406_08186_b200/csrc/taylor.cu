@@ -36,33 +36,13 @@ constexpr int kTermBlocks = 2048;   // fixed grid => deterministic partial order
 constexpr int kTermThreads = 256;
 constexpr int kPartialsMax = 16384;  // partial-sum slots in the evolve workspace
 
-// Programmatic dependent launch (PDL) around the term chain: wait until the
-// previous kernel in the stream has completed and its writes are visible (the
-// `done` flag included), then let the next one be scheduled so its launch
-// latency hides behind this kernel.  Both are no-ops without the attribute.
-__device__ __forceinline__ void pdl_enter() {
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-}
-
-// launch with the PDL attribute (QWB_TERM_PDL=0 turns it off)
+// Term chain launches (term -> finalize -> term ...) use programmatic
+// dependent launch (qwb::launch_pdl; QWB_TERM_PDL=0 turns it off).
+using qwb::pdl_enter;
 template <class... P, class... A>
 cudaError_t launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... args) {
-  static int pdl = [] {
-    const char* e = getenv("QWB_TERM_PDL");
-    return (e && *e) ? atoi(e) : 1;
-  }();
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
+  static const bool pdl = qwb::env_flag("QWB_TERM_PDL", 1) != 0;
+  return qwb::launch_pdl(pdl, kernel, grid, block, smem, s, std::forward<A>(args)...);
 }
 
 // Streaming x0 + pairwise(x1..x{L-1}) for rows of L <= 65 entries, element by
