@@ -274,7 +274,7 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
   // programmatic dependent launch: everything above overlaps the previous
   // launch's last tiles; its output (this launch's input) is visible after the
   // wait (a no-op when launched without the PDL attribute)
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  qwb::pdl_wait();
   int tile = blockIdx.x + tile0;   // tile0 > 0: a launch over tiles [tile0, ntiles) only
   if (tile >= ntiles) return;
   int tcol = tile % tiles_x, trow = tile / tiles_x;
@@ -300,7 +300,7 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
   for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
     // last tile of this CTA: let the next launch's CTAs take the SMs that
     // finish first (they block in griddepcontrol.wait until this grid is done)
-    if (tile + (int)gridDim.x >= ntiles) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    if (tile + (int)gridDim.x >= ntiles) qwb::pdl_trigger();
     const int k = S::NSTAGE == 2 ? (it & 1) : 0;
     double2* stage = stage0 + (size_t)k * 4 * S::REG;
     // x0: global column of the tile's first owned column; y0: unwrapped
@@ -443,19 +443,10 @@ int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const TbGeo& geo, 
       if (e != cudaSuccess) return qwb::cuda_status(ctx, e, "cudaFuncSetAttribute(lattice_tb)");
       configured[dev] = true;
     }
-    static int pdl = env_int("QWB_LATTICE_PDL", 1);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid_ ? grid_ : grid);
-    cfg.blockDim = dim3(32, BY);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, nx, ny, geo, in, out, bits, mk, tr, tiles_x,
-                                             ntiles_ ? ntiles_ : ntiles, tile0, imap, use_tma);
+    static const bool pdl = env_int("QWB_LATTICE_PDL", 1) != 0;   // see qwb::launch_pdl
+    const cudaError_t e = qwb::launch_pdl(pdl, kernel, dim3(grid_ ? grid_ : grid), dim3(32, BY), smem, s, nx, ny,
+                                          geo, in, out, bits, mk, tr, tiles_x, ntiles_ ? ntiles_ : ntiles, tile0,
+                                          imap, use_tma);
     if (e != cudaSuccess) return qwb::cuda_status(ctx, e, "cudaLaunchKernelEx(lattice_tb)");
     return QWB_OK;
   };
