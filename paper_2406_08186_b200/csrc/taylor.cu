@@ -479,8 +479,6 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
                  double* __restrict__ partial) {
   using namespace hcs;
   constexpr int VPT = TILE / CONS;
-  pdl_enter();
-  if (*done) return;
   extern __shared__ __align__(128) unsigned char hcs_smem[];
   double2* ring = reinterpret_cast<double2*>(hcs_smem);
   double2* accbuf = ring + (size_t)NS * TILE;                  // [2][TILE]
@@ -510,6 +508,8 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  pdl_enter();   // the barrier set-up above overlaps the previous kernel
+  if (*done) return;
 
   const int lane = tid & 31;
   const double2 alpha = make_double2(0.0, -s_k);      // Python complex(-1j * tau / k)
