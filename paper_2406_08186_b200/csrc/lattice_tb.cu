@@ -115,6 +115,64 @@ __device__ __forceinline__ double trace_p(int gx, int gy, int nx, int ny, double
   return __dadd_rn(m0, __dadd_rn(__dadd_rn(m1, m2), m3));
 }
 
+// Light-cone trace.  The traced vertex's amplitudes at levels 0..T-1 of a
+// T-step launch depend only on the (2T+1)^2 input vertices around it, so one
+// CTA per traced vertex recomputes that patch with the tile kernel's own
+// arithmetic (vertex_outputs2 in doubled space, the same pushes) and writes p
+// per level: bit-identical to the TRACE tile recompute, at a few microseconds
+// instead of a whole 32x64 tile.  Reads the launch's input, writes the trace
+// only.  Patch vertices whose neighbours fall outside the patch go stale one
+// ring per step; the centre stays exact for T steps.
+template <int SHIFT, int T>
+__global__ void __launch_bounds__(256)
+lattice_trace_cone_kernel(int nx, int ny, const double2* __restrict__ in, const uint32_t* __restrict__ bits,
+                          TraceList tr) {
+  constexpr int P = 2 * T + 1;
+  static_assert(P * P <= 256, "patch larger than the CTA");
+  __shared__ double2 o[4][P * P];
+  qwb::pdl_enter();
+  const int k = blockIdx.x;
+  if (k >= tr.n) return;
+  const int i = threadIdx.x;
+  const bool act = i < P * P;
+  const int px = i % P, py = i / P;
+  int cx = 0, cy = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)   // static indices: tr stays in the param space
+    if (j == k) {
+      cx = tr.x[j];
+      cy = tr.y[j];
+    }
+  const int gx = wrapc(cx - T + px, nx), gy = wrapc(cy - T + py, ny);
+  const int64_t n = (int64_t)nx * ny, w = (int64_t)gy * nx + gx;
+  double2 v[4] = {};
+  bool mk = false;
+  if (act) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p) v[p] = in[p * n + w];
+    if (bits) mk = (__ldg(bits + (w >> 5)) >> (w & 31)) & 1u;
+  }
+  const bool centre = act && px == T && py == T;
+#pragma unroll 1
+  for (int t = 0; t < T; ++t) {
+    if (centre) tr.out[t * tr.n + k] = trace_p(gx, gy, nx, ny, 1.0 / (double)(1 << t), v);
+    if (act) qwb::vertex_outputs2(gx, gy, nx, ny, mk, v[0], v[1], v[2], v[3], o[0][i], o[1][i], o[2][i], o[3][i]);
+    __syncthreads();
+    if (act) {
+      const double2 fromRight = o[1][px + 1 < P ? i + 1 : i];   // O_L of (x+1, y)
+      const double2 fromLeft = o[2][px > 0 ? i - 1 : i];        // O_R of (x-1, y)
+      const double2 fromAbove = o[0][py + 1 < P ? i + P : i];   // O_D of (x, y+1)
+      const double2 fromBelow = o[3][py > 0 ? i - P : i];       // O_U of (x, y-1)
+      if (SHIFT == QWB_SHIFT_FLIPFLOP) {
+        v[3] = fromAbove; v[0] = fromBelow; v[2] = fromRight; v[1] = fromLeft;
+      } else {
+        v[0] = fromAbove; v[3] = fromBelow; v[1] = fromRight; v[2] = fromLeft;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // T steps of a tile on chip (see the file comment).  INTERIOR: every vertex of
 // the region is an unmarked, untraced interior vertex (no slot permutation, no
 // branches).  TRACE: record the level-t amplitudes of the traced vertices this
@@ -459,10 +517,20 @@ int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const TbGeo& geo, 
       QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "slab kernels exist for T = %d on 32x64 regions only", kSlabDepth);
     }
   }
-  static int trace_split = env_int("QWB_LATTICE_TRACE_SPLIT", 1);
+  // QWB_LATTICE_TRACE_SPLIT: 2 (default) light-cone trace kernel after the
+  // plain launch, 1 TRACE tile recompute per traced tile, 0 trace fused into
+  // the full launch (the last two measured slower: DESIGN.md §4)
+  static int trace_split = env_int("QWB_LATTICE_TRACE_SPLIT", 2);
   if (tr.n > 0 && !trace_split) return go(lattice_tb_kernel<SHIFT, MARKED, T, BY, V, true, false>, conf_trace);
   int st = go(lattice_tb_kernel<SHIFT, MARKED, T, BY, V, false, false>, conf_plain);
   if (st || tr.n == 0) return st;
+  if (trace_split == 2) {
+    static const bool pdl = env_int("QWB_LATTICE_PDL", 1) != 0;
+    const cudaError_t e = qwb::launch_pdl(pdl, lattice_trace_cone_kernel<SHIFT, T>, dim3(tr.n), dim3(256), 0, s,
+                                          nx, ny, in, MARKED ? bits : nullptr, tr);
+    if (e != cudaSuccess) return qwb::cuda_status(ctx, e, "lattice_trace_cone_kernel");
+    return QWB_OK;
+  }
   // Traced run: the plain launch above advanced every tile; the tiles that own
   // a traced vertex are then recomputed from the same input (still intact: the
   // output is the other buffer) by the TRACE instantiation, one CTA each, which
