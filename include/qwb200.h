@@ -124,7 +124,9 @@ int qwb_spmv(qwb_ctx* ctx, int64_t n_rows, const int64_t* row_offsets, const int
 /* Repeated SpMV: the coined.simulate loop (coined.py:263-272).  Writes
  * snapshots U^{k_j} psi0 for the non-decreasing step counts k_host[0..n_snap)
  * into snaps[j * n_rows ...].  Small operators run the whole loop in one
- * persistent CTA with the state in shared memory.  scratch: 2*n_rows qwb_z. */
+ * persistent CTA with the state in shared memory.  scratch: 2*n_rows + 1 qwb_z
+ * (the second vector starts at an even offset).  Any pointer alignment is
+ * accepted; 32-B aligned val / scratch take the 256-bit load path. */
 int qwb_csr_run(qwb_ctx* ctx, int64_t n_rows, const int64_t* row_offsets, const int32_t* col,
                 const qwb_z* val, const qwb_z* psi0, const int64_t* k_host, int64_t n_snap,
                 qwb_z* snaps, qwb_z* scratch, void* stream);

@@ -258,7 +258,7 @@ class _CsrRunner:
         self.u = device_operator(engine, spec.graph, spec.shift, spec.active_marked)
         self.n = self.u.n_rows
         self.cur = empty_z(engine, self.n)
-        self.scratch = empty_z(engine, 2 * self.n)
+        self.scratch = empty_z(engine, 2 * self.n + 1)
 
     def load(self, arcs):
         self.cur.copy_(arcs)

@@ -39,6 +39,23 @@ int begin(qwb_ctx* ctx) {
 }
 
 int workspace(qwb_ctx* ctx, size_t bytes, cudaStream_t s, void** out) {
+  if (ctx->ws && s != ctx->ws_stream) {
+    // the previous user's stream may still run kernels on the workspace
+    if (!ctx->ws_event) {
+      cudaError_t e = cudaEventCreateWithFlags(&ctx->ws_event, cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_status(ctx, e, "cudaEventCreate(workspace)");
+    }
+    cudaError_t e = cudaEventRecord(ctx->ws_event, ctx->ws_stream);
+    if (e == cudaSuccess) {
+      e = cudaStreamWaitEvent(s, ctx->ws_event, 0);
+    } else {
+      // the previous stream is gone (destroyed by its owner): drain the device
+      cudaGetLastError();
+      e = cudaDeviceSynchronize();
+    }
+    if (e != cudaSuccess) return cuda_status(ctx, e, "workspace stream ordering");
+  }
+  ctx->ws_stream = s;
   bytes = (bytes + 255) & ~size_t(255);
   if (bytes < 256) bytes = 256;
   if (ctx->ws_bytes < bytes) {
@@ -99,6 +116,8 @@ int qwb_init(int device, qwb_ctx** out) {
   c->stopped = false;
   c->ws = nullptr;
   c->ws_bytes = 0;
+  c->ws_stream = nullptr;
+  c->ws_event = nullptr;
   c->pinned = nullptr;
   c->comm = nullptr;
   c->nranks = 1;
@@ -129,6 +148,8 @@ int qwb_shutdown(qwb_ctx* ctx) {
   cudaDeviceSynchronize();
   if (ctx->comm) qwb_comm_destroy(ctx);
   if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->ws_event) cudaEventDestroy(ctx->ws_event);
+  ctx->ws_event = nullptr;
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   ctx->ws = nullptr;
   ctx->pinned = nullptr;

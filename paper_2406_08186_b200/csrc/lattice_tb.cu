@@ -697,8 +697,9 @@ int launch_wf(qwb_ctx* ctx, int shift, cudaStream_t s, int nx, int ny, const dou
 namespace qwb {
 
 // Steps per temporally blocked launch (0 = single-step kernel only).
-// QWB_LATTICE_T overrides (0, 2..8); QWB_LATTICE_KIND picks the wavefront
-// ("wf", default) or the CTA-tile ("tile") variant; QWB_LATTICE_SHAPE the tile shape.
+// QWB_LATTICE_T overrides (0, 2..8); QWB_LATTICE_KIND picks the CTA-tile
+// variant (default) or, with "wf", the wavefront variant (opt-in A/B switch);
+// QWB_LATTICE_SHAPE the tile shape.
 int lattice_kind() {   // 1 = CTA tile (default), 0 = wavefront
   static int kind = -1;
   if (kind < 0) {

@@ -15,9 +15,14 @@ struct qwb_ctx {
   int device;
   int num_sms;
   bool stopped;
-  // stream-ordered scratch (grown on demand)
+  // stream-ordered scratch (grown on demand).  ws_stream: the stream of the
+  // last call that used it; a call on another stream first waits for the
+  // work queued there (ws_event), so neither reuse nor cudaFreeAsync on
+  // growth can overlap an earlier kernel that still reads or writes it.
   void* ws;
   size_t ws_bytes;
+  cudaStream_t ws_stream;
+  cudaEvent_t ws_event;
   // pinned host staging for small readbacks
   void* pinned;
   std::string last_error;

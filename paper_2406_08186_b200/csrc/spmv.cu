@@ -58,7 +58,13 @@ __device__ __forceinline__ double2 row_value(const G& g, int64_t len) {
   return qwb::reduceat_z(g, len);
 }
 
-// two consecutive complex128 (32 B, 32-B aligned) in one 256-bit load
+// two consecutive complex128 (32 B, 32-B aligned) in one 256-bit load.  The
+// kernel takes this path only when the caller's val and x are 32-B aligned
+// (`vec`, checked on the host: any pointer is legal at the C ABI)
+__host__ __forceinline__ int vec_ok(const void* val, const void* x) {
+  return (((uintptr_t)val | (uintptr_t)x) & 31) == 0;
+}
+
 __device__ __forceinline__ void ld2z(const double2* p, double2& a, double2& b) {
   asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
       : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
@@ -68,12 +74,12 @@ __device__ __forceinline__ void ld2z(const double2* p, double2& a, double2& b) {
 __global__ void __launch_bounds__(256)
 spmv_kernel(int64_t n_rows, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
             const double2* __restrict__ val, const double2* __restrict__ x,
-            double2* __restrict__ y) {
+            double2* __restrict__ y, int vec) {
   qwb::pdl_enter();   // x is the previous launch's y in the step loop
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_rows;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = __ldg(rowptr + r), e = __ldg(rowptr + r + 1);
-    if (e - s == 4 && (s & 3) == 0) {
+    if (vec && e - s == 4 && (s & 3) == 0) {
       // 4-entry row (every Grover row of a degree-4 head): one 128-bit column
       // load, two 256-bit value loads; the columns are the head's arc span, so
       // x usually comes in two 256-bit loads as well
@@ -194,7 +200,7 @@ int qwb_spmv(qwb_ctx* ctx, int64_t n_rows, const int64_t* row_offsets, const int
   static const bool pdl = qwb::env_flag("QWB_STEP_PDL", 1) != 0;   // see qwb::launch_pdl
   qwb::launch_pdl(pdl, spmv_kernel, qwb::blocks_for(n_rows, 256, (int64_t)ctx->num_sms * 64), 256, 0,
                   qwb::as_stream(stream), n_rows, row_offsets, col, reinterpret_cast<const double2*>(val),
-                  reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y));
+                  reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y), vec_ok(val, x));
   QWB_LAUNCH_CHECK(ctx, "spmv_kernel");
   return QWB_OK;
 }
@@ -230,8 +236,11 @@ int qwb_csr_run(qwb_ctx* ctx, int64_t n_rows, const int64_t* row_offsets, const 
     QWB_CUDA(ctx, cudaStreamSynchronize(s));
     return QWB_OK;
   }
+  // scratch holds 2 n_rows + 1 entries: b starts at an even offset so both
+  // ping-pong vectors keep the scratch's 32-B alignment
   double2* a = reinterpret_cast<double2*>(scratch);
-  double2* b = a + n_rows;
+  double2* b = a + ((n_rows + 1) & ~(int64_t)1);
+  const int vec = vec_ok(val, a) && vec_ok(val, b);
   QWB_CUDA(ctx, cudaMemcpyAsync(a, psi0, n_rows * sizeof(double2), cudaMemcpyDeviceToDevice, s));
   const unsigned grid = qwb::blocks_for(n_rows, 256, (int64_t)ctx->num_sms * 64);
   static const bool pdl = qwb::env_flag("QWB_STEP_PDL", 1) != 0;   // see qwb::launch_pdl
@@ -239,7 +248,7 @@ int qwb_csr_run(qwb_ctx* ctx, int64_t n_rows, const int64_t* row_offsets, const 
   for (int64_t j = 0; j < n_snap; ++j) {
     for (; cur < k_host[j]; ++cur) {
       qwb::launch_pdl(pdl, spmv_kernel, grid, 256, 0, s, n_rows, row_offsets, col, v,
-                      (const double2*)a, b);
+                      (const double2*)a, b, vec);
       double2* t = a;
       a = b;
       b = t;

@@ -295,6 +295,10 @@ def _init_comm(engine: Engine, rank: int, world: int, group=None) -> None:
     dist.broadcast_object_list(obj, src=0, group=group)
     uid = C.create_string_buffer(obj[0], 128)
     engine.call("qwb_comm_init", uid, world, rank)
+    if os.environ.get("QWB_LOG_COMM"):
+        import sys
+        print(f"qwb: NCCL communicator initialised: rank {rank} nranks {world} device {engine.device}",
+              file=sys.stderr, flush=True)
 
 
 def _hypercube_setup(engine: Engine, dim: int, gamma: float, marked):
@@ -329,6 +333,10 @@ class ShardedHypercubeWalk:
         self.lo, self.hi = hypercube_shard(self.dim, self.world, self.rank)
         self.n_local = self.hi - self.lo
         self.group = group
+        if self.world > 1 and not self.comm:
+            # the single-GPU kernel needs the whole 2^dim state; a shard holds
+            # 2^(dim-S) entries (emulate_hypercube_shards runs shards locally)
+            raise ValueError("ShardedHypercubeWalk with world > 1 needs comm=True")
         self.bits, self.inf_norm = _hypercube_setup(engine, self.dim, self.gamma, marked)
         self.work = empty_z(engine, (3 + self.S) * self.n_local)
         if self.comm:

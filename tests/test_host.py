@@ -155,3 +155,24 @@ def test_family_closed_forms_match_oracle():
     c = 4096 + 8192 * 4096
     assert q.graphs.arc_index(q.graphs.arc_basis(big), c, c + 1) == 4 * c + 2
     assert big._adjacency is None
+
+
+def test_bench_refuses_more_gpus_than_visible():
+    """`bench.py --gpus N` re-execs itself under torchrun when N > 1 and no
+    WORLD_SIZE is set, but only when N GPUs are visible: here (no GPU) it must
+    fail loudly instead of measuring one GPU and reporting it as N."""
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1",
+                        "--warmup", "3", "--no-extras", "--no-cpu"], capture_output=True, text=True, env=env,
+                       timeout=300)
+    assert r.returncode != 0
+    assert "2 requested but 0 CUDA device" in r.stderr
+    # a torchrun world that disagrees with --gpus is refused as well
+    env.update(WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 2 and "WORLD_SIZE=1" in r.stderr
