@@ -340,10 +340,12 @@ def run_b200(args):
     N.load().qwb_lattice_fused_depth(nx, nx, 0, C.byref(dep), C.byref(knd))
     if single:
         depth = dep.value
-        if depth > 0:
+        if depth > 0 and knd.value == 2:
+            per_walk = 1 + walk % depth   # one persistent flow launch + remainder single steps
+            kernel = f"lattice_flow_kernel<flipflop, T={depth}, 32x64 region> (persistent, {walk // depth} blocks)"
+        elif depth > 0:
             per_walk = walk // depth + walk % depth
-            kernel = (f"lattice_tb_kernel<flipflop, T={depth}, 32x64 region>" if knd.value == 1
-                      else f"lattice_wf_kernel<flipflop, T={depth}>")
+            kernel = f"lattice_tb_kernel<flipflop, T={depth}, 32x64 region>"
         else:
             per_walk = walk
             kernel = "lattice_step_kernel<flipflop>"

@@ -156,8 +156,10 @@ int qwb_lattice_run(qwb_ctx* ctx, int64_t nx, int64_t ny, int shift, const uint3
                     const int64_t* trace_vertices_host, int n_trace, double* trace,
                     int* final_in_b_host, void* stream);
 /* Coined steps fused per HBM pass by qwb_lattice_run for this lattice (0 =
- * one step per launch) and the fused kernel kind (1 = CTA tile, 0 = wavefront).
- * Environment overrides: QWB_LATTICE_T, QWB_LATTICE_KIND, QWB_LATTICE_SHAPE.  */
+ * one step per launch) and how an untraced run launches it (2 = one
+ * persistent dataflow launch for the whole run, 1 = one tile launch per T
+ * steps).  Environment overrides: QWB_LATTICE_T, QWB_LATTICE_SHAPE,
+ * QWB_LATTICE_FLOW.                                                          */
 int qwb_lattice_fused_depth(int64_t nx, int64_t ny, int64_t n_marked, int* depth_host, int* kind_host);
 /* One step with an optional fused full distribution p of the INPUT state.    */
 int qwb_lattice_step(qwb_ctx* ctx, int64_t nx, int64_t ny, int shift, const uint32_t* marked_bits,

@@ -118,6 +118,7 @@ int qwb_init(int device, qwb_ctx** out) {
   c->ws_bytes = 0;
   c->ws_stream = nullptr;
   c->ws_event = nullptr;
+  c->lat_sticky = nullptr;
   c->pinned = nullptr;
   c->comm = nullptr;
   c->nranks = 1;
@@ -150,6 +151,8 @@ int qwb_shutdown(qwb_ctx* ctx) {
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->ws_event) cudaEventDestroy(ctx->ws_event);
   ctx->ws_event = nullptr;
+  if (ctx->lat_sticky) cudaFree(ctx->lat_sticky);
+  ctx->lat_sticky = nullptr;
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   ctx->ws = nullptr;
   ctx->pinned = nullptr;

@@ -367,13 +367,36 @@ int qwb_lattice_run(qwb_ctx* ctx, int64_t nx, int64_t ny, int shift, const uint3
   // T coined steps per HBM pass when no per-step trace is requested
   if (n_marked > 0 && (!marked_bits || !marked_host))
     QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "marked vertices need both the bitmap and the host list");
-  // the tile kernel fuses the per-step trace too; the wavefront kernel does not
-  const int depth = (trace && qwb::lattice_kind() == 0) ? 0 : qwb::lattice_tb_depth(nx, ny, n_marked);
-  if (depth > 0) {
-    for (; k + depth <= steps; k += depth) {
+  const int depth = qwb::lattice_tb_depth(nx, ny, n_marked);
+  // untraced runs: one persistent dataflow launch for all whole T-step blocks
+  const int nflow = depth > 0 ? qwb::lattice_flow_blocks(nx, ny, depth, trace != nullptr, steps, ctx->num_sms) : 0;
+  if (nflow > 0) {
+    st = qwb::lattice_flow_launch(ctx, shift, s, (int)nx, (int)ny, cur, nxt, marked_bits, marked_host, n_marked,
+                                  nflow);
+  }
+  if (nflow > 0 && st == -1) {   // no co-resident grid here: one launch per T steps
+    st = QWB_OK;
+  } else if (nflow > 0) {
+    if (st) return st;
+    k = (int64_t)nflow * depth;
+    if (nflow & 1) {
+      double2* t = cur;
+      cur = nxt;
+      nxt = t;
+    }
+    swaps += nflow;
+  }
+  if (depth > 0 && k + depth <= steps) {
+    // subnormal guard: the first launch and every kCheckEvery-th test the
+    // tiles' inputs; a hit switches the rest of the run to numpy's arithmetic
+    int* sticky = nullptr;
+    st = qwb::lattice_sticky(ctx, &sticky);
+    if (st) return st;
+    QWB_CUDA(ctx, cudaMemsetAsync(sticky, 0, sizeof(int), s));
+    for (int64_t i = 0; k + depth <= steps; k += depth, ++i) {
       st = qwb::lattice_tb_launch(ctx, depth, shift, s, (int)nx, (int)ny, cur, nxt, marked_bits,
                                   marked_host, n_marked, trace_vertices_host, trace ? n_trace : 0,
-                                  trace ? trace + k * n_trace : nullptr);
+                                  trace ? trace + k * n_trace : nullptr, i % qwb::kCheckEvery == 0, sticky);
       if (st) return st;
       double2* t = cur;
       cur = nxt;
@@ -531,7 +554,7 @@ int qwb_slab_advance_local(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int
     QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "ext = %d leaves fewer than %d ghost rows", ext, T);
   const qwb::TbGeo geo{(int)(ny_local + 2 * ghost), (int)ghost - ext, (int)ny_local + 2 * ext, (int)y0 - ext, 0};
   st = qwb::lattice_tb_launch_geo(ctx, T, shift, s, (int)nx, (int)ny, geo, x, y, marked_bits, marked_host,
-                                  n_marked);
+                                  n_marked, 0, 0);
   if (st) return st;
   QWB_LAUNCH_CHECK(ctx, "lattice_tb_kernel(ghost slab)");
   return QWB_OK;

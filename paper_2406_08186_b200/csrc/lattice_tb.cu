@@ -7,25 +7,40 @@
 // owns V vertically adjacent vertices with their 4 direction amplitudes in
 // registers:
 //
-//   * the region's state arrives in shared memory one or two tiles ahead of its
-//     use, so HBM reads overlap the arithmetic of the current tile: regions
-//     inside the buffer with ONE tensor TMA (box [4 planes][BY*V rows][32]
-//     complex128, completion on a stage mbarrier), regions that wrap around
-//     the torus with per-thread 16-B cp.async;
+//   * the region's state arrives in shared memory one tile ahead of its use,
+//     so HBM reads overlap the arithmetic of the current tile: regions inside
+//     the buffer with ONE tensor TMA (box [4 planes][BY*V rows][32]
+//     complex128, completing on the stage's mbarrier), regions that wrap
+//     around the torus with per-thread 16-B cp.async;
 //   * T steps run on chip, in doubled space (qwb_lattice.cuh "doubled-space
 //     forms": the operator 2U needs additions only — 20 FP64 adds per vertex
 //     and step — and the state is scaled by 2^-T on the way out, so the result
-//     has numpy's bits for every non-zero amplitude).  Pushes to x +- 1 go
-//     through warp shuffles (a warp is one region row of 32 columns), pushes
-//     between a thread's own V rows stay in registers, and only the pushes
-//     across thread rows go through a double-buffered shared-memory exchange
-//     (one barrier per step);
+//     has numpy's bits).  A tile whose input holds a non-zero amplitude below
+//     2^-1016 (checked on the loaded registers) runs the same steps in EXACT
+//     mode (numpy's halving first), which keeps the bits in the subnormal
+//     range too.  Pushes to x +- 1 go through warp shuffles (a warp is one
+//     region row of 32 columns), pushes between a thread's own V rows stay in
+//     registers, and only the pushes across thread rows go through a
+//     double-buffered shared-memory exchange (one barrier per step);
 //   * values near the region edge go stale one ring per step, so after T steps
 //     the inner (32 - 2T) x (BY*V - 2T) vertices are exact and are written.
 //
+// Two launch forms:
+//   * lattice_tb_kernel — one launch per T steps over all tiles (persistent
+//     CTAs, static tile order).  Used for traced search runs (the light-cone
+//     trace kernel reads each launch's input) and for multi-GPU y-slabs with
+//     ghost state rows (SLAB, TbGeo: owned rows only, no y-wrap; comm.cu).
+//   * lattice_flow_kernel — ONE launch for a whole run of K x T steps on the
+//     torus.  Work items (block k, tile) are taken in order from a global
+//     counter; an item waits until the tiles whose owned cells its region
+//     reads have finished block k - 1 (per-tile progress counters,
+//     release / acquire), so block k + 1 starts on a tile while other tiles
+//     still finish block k.  No launch gap, no pipeline refill and no tail per
+//     T steps; the tile-row order rotates by half the torus every block so an
+//     item's dependencies are ~half a block old.  Items depend only on earlier
+//     items, so the schedule cannot deadlock whatever the CTA residency.
+//
 // Regions wrap around the torus (modular global coordinates): any nx, ny >= 3.
-// The same kernel runs on multi-GPU y-slabs with ghost state rows (SLAB,
-// TbGeo): owned rows only, no y-wrap (comm.cu qwb_slab_run_fused).
 // Default tile: 16 warps x 4 rows (32 x 64 region), T = 4.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -37,21 +52,13 @@ namespace {
 
 using qwb::TbGeo;
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void tb_mbar_init(uint64_t* b, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count)
-               : "memory");
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
 }
 __device__ __forceinline__ void tb_mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
-                   (unsigned)__cvta_generic_to_shared(b)),
-               "r"(bytes)
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes)
                : "memory");
 }
 __device__ __forceinline__ void tb_mbar_wait(uint64_t* b, uint32_t parity) {
@@ -61,9 +68,27 @@ __device__ __forceinline__ void tb_mbar_wait(uint64_t* b, uint32_t parity) {
       "TB_WAIT_%=:\n"
       " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra TB_WAIT_%=;\n"
-      "}\n" ::"r"((unsigned)__cvta_generic_to_shared(b)),
+      "}\n" ::"r"(smem_u32(b)),
       "r"(parity)
       : "memory");
+}
+// progress counters of the flow kernel
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+#ifdef QWB_EXP_LDACQ
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+#else
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+#endif
+  return v;
+}
+// after observing the counters with relaxed loads: acquire, then order the
+// async proxy (TMA / bulk copies) after it
+__device__ __forceinline__ void acquire_for_async() {
+#if !defined(QWB_EXP_NOFENCE) && !defined(QWB_EXP_LDACQ)
+  asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+#endif
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
 }
 
 __device__ __forceinline__ int wrapc(int v, int n) {
@@ -79,7 +104,6 @@ __device__ __forceinline__ double2 shfl_up2(double2 v) {
 }
 
 using qwb::kSlabDepth;
-constexpr size_t kTraceRecBytes = 6 * 8 * 4 * sizeof(double2);   // [T <= 6][8 vertices][4 planes]
 
 template <int BY, int V>
 struct TbShape {
@@ -89,12 +113,12 @@ struct TbShape {
   static constexpr int REG = RX * RY;      // region vertices
   // stages of the next tiles' amplitudes: two (loads of two tiles in flight)
   // when they fit next to the exchange buffers, else one
-  static constexpr int NSTAGE =
-      ((8 * (size_t)REG + 4 * (size_t)NT) * sizeof(double2) + 16 + kTraceRecBytes <= 232448) ? 2 : 1;
-  static constexpr size_t smem_bytes() {   // + two mbarriers for the TMA loads + the trace record
-    return (4 * (size_t)REG * NSTAGE + 4 * (size_t)NT) * sizeof(double2) + 2 * sizeof(uint64_t) +
-           kTraceRecBytes;
+  static constexpr int NSTAGE = ((8 * (size_t)REG + 4 * (size_t)NT) * sizeof(double2) + 64 <= 232448) ? 2 : 1;
+  static constexpr size_t smem_bytes() {   // stages + exchange + two mbarriers + scheduling words
+    return (4 * (size_t)REG * NSTAGE + 4 * (size_t)NT) * sizeof(double2) + 2 * sizeof(uint64_t) + kSchedBytes;
   }
+  // flow kernel: 2 item words + 32 dependency pointers and block counts
+  static constexpr size_t kSchedBytes = 16 + 32 * sizeof(void*) + 32 * sizeof(unsigned);
 };
 
 // p(v) per step for up to 8 traced vertices (search runs): out[t * n + k];
@@ -106,8 +130,15 @@ struct TraceList {
   double* out;
 };
 
-// p of a traced vertex from its level-t (doubled-space) amplitudes a[0..3]
-// (planes D, L, R, U): unscale, reference slot order, numpy |z|^2, row sum.
+struct MarkedList {   // up to 8 marked vertex ids; n < 0: more than 8 (use the bitmap)
+  int n;
+  int64_t v[8];
+  int x[8], y[8];     // their coordinates (host-computed)
+};
+
+// p of a traced vertex from its level-t amplitudes a[0..3] (planes D, L, R,
+// U; sc undoes the doubled-space scale): reference slot order, numpy |z|^2,
+// row sum.
 __device__ __forceinline__ double trace_p(int gx, int gy, int nx, int ny, double sc, const double2* a) {
   const auto un = [&](double2 z) { return make_double2(__dmul_rn(z.x, sc), __dmul_rn(z.y, sc)); };
   const qwb::Slots o = qwb::order_slots(gx, gy, nx, ny, un(a[0]), un(a[1]), un(a[2]), un(a[3]));
@@ -118,11 +149,12 @@ __device__ __forceinline__ double trace_p(int gx, int gy, int nx, int ny, double
 // Light-cone trace.  The traced vertex's amplitudes at levels 0..T-1 of a
 // T-step launch depend only on the (2T+1)^2 input vertices around it, so one
 // CTA per traced vertex recomputes that patch with the tile kernel's own
-// arithmetic (vertex_outputs2 in doubled space, the same pushes) and writes p
-// per level: bit-identical to the TRACE tile recompute, at a few microseconds
-// instead of a whole 32x64 tile.  Reads the launch's input, writes the trace
-// only.  Patch vertices whose neighbours fall outside the patch go stale one
-// ring per step; the centre stays exact for T steps.
+// arithmetic (vertex_outputs2, the same pushes; exact mode when the patch
+// holds a non-zero amplitude below 2^-1016) and writes p per level: numpy's
+// values, at a few microseconds instead of a whole 32x64 tile.  Reads the
+// launch's input, writes the trace only.  Patch vertices whose neighbours
+// fall outside the patch go stale one ring per step; the centre stays exact
+// for T steps.
 template <int SHIFT, int T>
 __global__ void __launch_bounds__(256)
 lattice_trace_cone_kernel(int nx, int ny, const double2* __restrict__ in, const uint32_t* __restrict__ bits,
@@ -147,16 +179,22 @@ lattice_trace_cone_kernel(int nx, int ny, const double2* __restrict__ in, const 
   const int64_t n = (int64_t)nx * ny, w = (int64_t)gy * nx + gx;
   double2 v[4] = {};
   bool mk = false;
+  unsigned m = ~0u;
   if (act) {
 #pragma unroll
-    for (int p = 0; p < 4; ++p) v[p] = in[p * n + w];
+    for (int p = 0; p < 4; ++p) {
+      v[p] = in[p * n + w];
+      m = qwb::tiny_acc2(m, v[p]);
+    }
     if (bits) mk = (__ldg(bits + (w >> 5)) >> (w & 31)) & 1u;
   }
+  const bool exact = __syncthreads_or(m < qwb::kTinyKey);
   const bool centre = act && px == T && py == T;
 #pragma unroll 1
   for (int t = 0; t < T; ++t) {
-    if (centre) tr.out[t * tr.n + k] = trace_p(gx, gy, nx, ny, 1.0 / (double)(1 << t), v);
-    if (act) qwb::vertex_outputs2(gx, gy, nx, ny, mk, v[0], v[1], v[2], v[3], o[0][i], o[1][i], o[2][i], o[3][i]);
+    if (centre) tr.out[t * tr.n + k] = trace_p(gx, gy, nx, ny, exact ? 1.0 : 1.0 / (double)(1 << t), v);
+    if (act)
+      qwb::vertex_outputs2(gx, gy, nx, ny, mk, exact, v[0], v[1], v[2], v[3], o[0][i], o[1][i], o[2][i], o[3][i]);
     __syncthreads();
     if (act) {
       const double2 fromRight = o[1][px + 1 < P ? i + 1 : i];   // O_L of (x+1, y)
@@ -173,52 +211,51 @@ lattice_trace_cone_kernel(int nx, int ny, const double2* __restrict__ in, const 
   }
 }
 
-// T steps of a tile on chip (see the file comment).  INTERIOR: every vertex of
-// the region is an unmarked, untraced interior vertex (no slot permutation, no
-// branches).  TRACE: record the level-t amplitudes of the traced vertices this
-// tile owns (the exact inner block) in trbuf[t][k][4]; p is computed after
-// the steps (no call and no extra registers in the step loop).
-template <int SHIFT, bool MARKED, int T, int BY, int V, bool INTERIOR, bool TRACE>
-__device__ __forceinline__ void tile_steps(int nx, int ny, int gx, const int (&gy)[V],
+// T steps of a tile on chip (see the file comment).  INTERIOR: no row of the
+// region is a torus edge row (y = 0, ny - 1) and no marked vertex lies in it:
+// one formula for every vertex (x-edge vertices included, qwb_lattice.cuh),
+// no per-vertex branch.  exact: numpy's per-step arithmetic (tiny inputs).
+//
+// The first step's barrier also ORs the threads' tiny-input flags (m, from
+// stage_to_regs): the result says whether the doubled-space attempt is
+// numpy's (false) or must be redone in EXACT mode (true; tile_run).
+// after0() runs right after the first step's barrier (the flow kernel issues
+// a wrapping next region's copies there).
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+template <int SHIFT, bool MARKED, int T, int BY, int V, bool INTERIOR, bool EXACT, class F>
+__device__ __forceinline__ bool tile_steps(int nx, int ny, int gx, const int (&gy)[V], unsigned m, unsigned key,
                                            const uint32_t* __restrict__ bits, double2 (&vD)[V],
                                            double2 (&vL)[V], double2 (&vR)[V], double2 (&vU)[V],
-                                           double2* xD, double2* xU, int tid, int ty,
-                                           const TraceList& tr, const bool (&own)[V], double2* trbuf) {
+                                           double2* xD, double2* xU, int tid, int ty, const F& after0) {
+  bool tiny = false;
   bool mk[V];
 #pragma unroll
   for (int j = 0; j < V; ++j) {
     mk[j] = false;
-    if (MARKED) {
+    if (MARKED && !INTERIOR) {
       const int64_t wg = (int64_t)gy[j] * nx + gx;
       mk[j] = (__ldg(bits + (wg >> 5)) >> (wg & 31)) & 1u;
     }
   }
 #pragma unroll
   for (int t = 0; t < T; ++t) {
-    if (TRACE) {
-#pragma unroll
-      for (int j = 0; j < V; ++j) {
-        if (!own[j]) continue;
-        const int64_t wg = (int64_t)gy[j] * nx + gx;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {   // static indices: tr stays in the param space
-          if (k >= tr.n || tr.v[k] != wg) continue;
-          double2* a = trbuf + (t * 8 + k) * 4;   // level t holds 2^t psi_t
-          a[0] = vD[j];
-          a[1] = vL[j];
-          a[2] = vR[j];
-          a[3] = vU[j];
-        }
-      }
-    }
     double2 oD[V], oL[V], oR[V], oU[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) {
-      if (INTERIOR)
+      if (INTERIOR) {
+        if (EXACT) {
+          vD[j] = qwb::halve(vD[j]);
+          vL[j] = qwb::halve(vL[j]);
+          vR[j] = qwb::halve(vR[j]);
+          vU[j] = qwb::halve(vU[j]);
+        }
         qwb::vertex_outputs2_interior(vD[j], vL[j], vR[j], vU[j], oD[j], oL[j], oR[j], oU[j]);
-      else
-        qwb::vertex_outputs2(gx, gy[j], nx, ny, mk[j], vD[j], vL[j], vR[j], vU[j], oD[j], oL[j],
-                             oR[j], oU[j]);
+      } else {
+        qwb::vertex_outputs2(gx, gy[j], nx, ny, mk[j], EXACT, vD[j], vL[j], vR[j], vU[j], oD[j], oL[j], oR[j],
+                             oU[j]);
+      }
     }
     const int b = (t & 1) * 32 * BY;
     xD[b + tid] = oD[0];
@@ -229,7 +266,11 @@ __device__ __forceinline__ void tile_steps(int nx, int ny, int gx, const int (&g
       fromRight[j] = shfl_down2(oL[j]);   // O_L of (x+1, y)
       fromLeft[j] = shfl_up2(oR[j]);      // O_R of (x-1, y)
     }
-    __syncthreads();
+    if (!EXACT && t == 0)
+      tiny = __syncthreads_or(m < key);
+    else
+      __syncthreads();
+    if (t == 0) after0();
     double2 fromAbove[V], fromBelow[V];   // O_D of (x, y+1), O_U of (x, y-1)
 #pragma unroll
     for (int j = 0; j < V - 1; ++j) fromAbove[j] = oD[j + 1];
@@ -246,59 +287,192 @@ __device__ __forceinline__ void tile_steps(int nx, int ny, int gx, const int (&g
       }
     }
   }
+  return tiny;
 }
 
-struct MarkedList {   // up to 8 marked vertex ids; n < 0: more than 8 (use the bitmap)
-  int n;
-  int64_t v[8];
-  int x[8], y[8];     // their coordinates (host-computed)
-};
+// Region loads.  A region inside the buffer arrives with ONE tensor TMA
+// issued by thread 0, completing on the stage's mbarrier; a region that wraps
+// around the torus (or reaches past a slab buffer) with per-thread 16-B
+// cp.async (all threads; rows outside a slab buffer are skipped: they are
+// > T rows from every owned row, left stale), completing on the threads'
+// cp.async group.  bx: global column of region column 0 (< 0 or past nx:
+// wrap); by: local buffer row of region row 0.
+template <class S>
+__device__ __forceinline__ bool region_inside(int nx, int lrows, int bx, int by, bool use_tma) {
+  return use_tma && bx >= 0 && bx + S::RX <= nx && by >= 0 && by + S::RY <= lrows;
+}
+template <class S>
+__device__ __forceinline__ void tma_region(double2* stage, uint64_t* bar, const CUtensorMap* map, int bx, int by) {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // earlier LDS of this stage
+  tb_mbar_expect_tx(bar, 4u * S::REG * (uint32_t)sizeof(double2));
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(smem_u32(stage)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(2 * bx), "r"(by), "r"(0), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-// SLAB: the buffer is a y-slab with ghost rows (geo), else the whole torus
-template <int SHIFT, bool MARKED, int T, int BY, int V, bool TRACE, bool SLAB>
+template <class S, int V, bool SLAB>
+__device__ __forceinline__ void cp_region(double2* stage, const double2* in, int nx, int ny, int lrows, int bx,
+                                          int by, int tx, int ty) {
+  const int64_t n = (int64_t)nx * lrows;   // plane stride
+  const int gx = wrapc(bx + tx, nx);
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    const int ly = by + ty * V + j;
+    if (SLAB && (ly < 0 || ly >= lrows)) continue;
+    const int r = SLAB ? ly : wrapc(ly, ny);
+    const int64_t w = (int64_t)r * nx + gx;
+    const int li = (ty * V + j) * 32 + tx;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) cp_async16(stage + p * S::REG + li, in + p * n + w);
+  }
+}
+
+// Registers of a tile from its stage, with the tiny-amplitude test.
+template <class S, int V>
+__device__ __forceinline__ unsigned stage_to_regs(const double2* stage, int tx, int ty, double2 (&vD)[V],
+                                                  double2 (&vL)[V], double2 (&vR)[V], double2 (&vU)[V],
+                                                  bool check = true) {
+  unsigned m = ~0u;
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    const int li = (ty * V + j) * 32 + tx;
+    vD[j] = stage[li];
+    vL[j] = stage[S::REG + li];
+    vR[j] = stage[2 * S::REG + li];
+    vU[j] = stage[3 * S::REG + li];
+#ifndef QWB_EXP_NOCHECK
+    if (!check) continue;
+    m = qwb::tiny_acc2(m, vD[j]);
+    m = qwb::tiny_acc2(m, vL[j]);
+    m = qwb::tiny_acc2(m, vR[j]);
+    m = qwb::tiny_acc2(m, vU[j]);
+#endif
+  }
+  return m;
+}
+
+// Steps + store of one tile whose registers are loaded.  (x0, y0): global
+// column / unwrapped global row of its first owned vertex; lyb: local buffer
+// row of that row; rows_left: owned rows from y0 to the end of the launch's
+// owned range; m: the threads' tiny-input flags (stage_to_regs).  The steps
+// run in doubled space; if any input amplitude of the region is tiny (rare:
+// the front of a localized start after ~1000 steps) the region is reloaded
+// from `in` (intact during the tile: the launch writes the other buffer, and
+// a flow item's input region is not overwritten before the item is done) and
+// the steps are redone in numpy's arithmetic.  The check is off the critical
+// path: its integer work interleaves with the first step, its reduction rides
+// on that step's barrier.
+template <int SHIFT, bool MARKED, int T, int BY, int V, bool SLAB, class F>
+__device__ __forceinline__ void tile_run(int nx, int ny, int64_t n, int lrows, int x0, int y0, int lyb,
+                                         int rows_left, unsigned m, unsigned key, bool all_exact,
+                                         const double2* __restrict__ in,
+                                         const uint32_t* __restrict__ bits, const MarkedList& mk,
+                                         double2 (&vD)[V], double2 (&vL)[V], double2 (&vR)[V], double2 (&vU)[V],
+                                         double2* xD, double2* xU, double2* __restrict__ out, int tx, int ty,
+                                         int tid, const F& after0, int* sticky = nullptr) {
+  using S = TbShape<BY, V>;
+  constexpr int OX = S::RX - 2 * T, OY = S::RY - 2 * T;
+  const int gx = wrapc(x0 - T + tx, nx);
+  int gy[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) gy[j] = wrapc(y0 - T + ty * V + j, ny);
+  // regions with no torus edge row and no marked vertex: one formula
+  bool interior = y0 - T >= 1 && y0 - T + S::RY - 1 <= ny - 2;
+  if (MARKED && interior) {
+    if (mk.n < 0) {
+      interior = false;   // too many marked vertices for the list: general path
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int dx = wrapc(mk.x[k] - (x0 - T) + nx, nx), dy = mk.y[k] - (y0 - T);
+        interior &= (k >= mk.n) || !(dx < S::RX && dy >= 0 && dy < S::RY);
+      }
+    }
+  }
+  bool tiny = all_exact;
+  if (all_exact) {   // a run that met tiny amplitudes: numpy's arithmetic from the start
+    if (interior)
+      tile_steps<SHIFT, false, T, BY, V, true, true>(nx, ny, gx, gy, 0u, 0u, bits, vD, vL, vR, vU, xD, xU, tid, ty,
+                                                     after0);
+    else
+      tile_steps<SHIFT, MARKED, T, BY, V, false, true>(nx, ny, gx, gy, 0u, 0u, bits, vD, vL, vR, vU, xD, xU, tid,
+                                                       ty, after0);
+  } else {
+    tiny = interior ? tile_steps<SHIFT, false, T, BY, V, true, false>(nx, ny, gx, gy, m, key, bits, vD, vL, vR, vU, xD,
+                                                                      xU, tid, ty, after0)
+                    : tile_steps<SHIFT, MARKED, T, BY, V, false, false>(nx, ny, gx, gy, m, key, bits, vD, vL, vR, vU,
+                                                                        xD, xU, tid, ty, after0);
+  }
+#ifndef QWB_EXP_NOREDO
+  if (tiny && !all_exact) {
+    if (sticky && tid == 0) atomicOr(sticky, 1);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      const int ly = lyb - T + ty * V + j;   // local buffer row
+      const bool ok = !SLAB || (ly >= 0 && ly < lrows);
+      const int64_t w = (int64_t)(SLAB ? (ok ? ly : 0) : wrapc(ly, ny)) * nx + gx;
+      const double2 z = make_double2(0.0, 0.0);
+      vD[j] = ok ? in[w] : z;
+      vL[j] = ok ? in[n + w] : z;
+      vR[j] = ok ? in[2 * n + w] : z;
+      vU[j] = ok ? in[3 * n + w] : z;
+    }
+    if (interior)
+      tile_steps<SHIFT, false, T, BY, V, true, true>(nx, ny, gx, gy, 0u, 0u, bits, vD, vL, vR, vU, xD, xU, tid, ty,
+                                                     NoHook{});
+    else
+      tile_steps<SHIFT, MARKED, T, BY, V, false, true>(nx, ny, gx, gy, 0u, 0u, bits, vD, vL, vR, vU, xD, xU, tid, ty,
+                                                       NoHook{});
+  }
+#endif
+  const double sc = tiny ? 1.0 : 1.0 / (double)(1 << T);   // undo the doubled-space steps (exact)
+  const bool col_ok = tx >= T && tx < T + OX && x0 + tx - T < nx;
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    const int ly = ty * V + j;
+    if (col_ok && ly >= T && ly < T + OY && ly - T < rows_left) {
+      const int64_t w = (int64_t)(lyb - T + ly) * nx + gx;
+      __stcs(out + w, make_double2(__dmul_rn(vD[j].x, sc), __dmul_rn(vD[j].y, sc)));
+      __stcs(out + n + w, make_double2(__dmul_rn(vL[j].x, sc), __dmul_rn(vL[j].y, sc)));
+      __stcs(out + 2 * n + w, make_double2(__dmul_rn(vR[j].x, sc), __dmul_rn(vR[j].y, sc)));
+      __stcs(out + 3 * n + w, make_double2(__dmul_rn(vU[j].x, sc), __dmul_rn(vU[j].y, sc)));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// One launch = T steps over tiles [tile0, ntiles).  SLAB: the buffer is a
+// y-slab with ghost rows (geo), else the whole torus.
+// ---------------------------------------------------------------------------
+template <int SHIFT, bool MARKED, int T, int BY, int V, bool SLAB>
 __global__ void __launch_bounds__(32 * BY, 1)
 lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, double2* __restrict__ out,
-                  const uint32_t* __restrict__ bits, MarkedList mk, TraceList tr, int tiles_x,
-                  int ntiles, int tile0, const __grid_constant__ CUtensorMap imap, int use_tma) {
+                  const uint32_t* __restrict__ bits, MarkedList mk, int tiles_x, int ntiles, int tile0,
+                  const __grid_constant__ CUtensorMap imap, int use_tma, unsigned key, int* sticky) {
   using S = TbShape<BY, V>;
   constexpr int OX = S::RX - 2 * T, OY = S::RY - 2 * T;   // exact (owned) block
-  extern __shared__ double2 sm[];
-  double2* stage0 = sm;                // [NSTAGE][4][RY][RX] next tiles' amplitudes
+  extern __shared__ __align__(128) double2 sm[];
+  double2* stage0 = sm;                        // [NSTAGE][4][RY][RX] next tiles' amplitudes
   double2* xD = sm + 4 * S::REG * S::NSTAGE;   // [2][BY][32] O_D of each thread's lowest row
-  double2* xU = xD + 2 * S::NT;        // [2][BY][32] O_U of each thread's highest row
-  uint64_t* tbar = reinterpret_cast<uint64_t*>(xU + 2 * S::NT);   // [2] TMA-load barriers
-  double2* trbuf = reinterpret_cast<double2*>(tbar + 2);          // [T][8][4] traced amplitudes (TRACE)
+  double2* xU = xD + 2 * S::NT;                // [2][BY][32] O_U of each thread's highest row
+  uint64_t* tbar = reinterpret_cast<uint64_t*>(xU + 2 * S::NT);   // [2] stage barriers
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * 32 + tx;
   if (!SLAB) geo = TbGeo{ny, 0, ny, 0, 1};   // compile-time constants for the torus
-  // Tiles whose region lies inside the torus (no wrap) load all four planes
-  // with ONE tensor TMA (box [4][RY][32] complex128) completing on a stage
-  // mbarrier; regions that wrap use per-thread cp.async.
-  const bool tma = use_tma;
-  if (tma) {
-    if (tid == 0) {
-      tb_mbar_init(tbar, 1);
-      tb_mbar_init(tbar + 1, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
+  if (tid == 0) {
+    tb_mbar_init(tbar, 1);
+    tb_mbar_init(tbar + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  auto tma_ok = [&](int tcol, int trow) {   // the region lies inside the buffer (no wrap)
-    const int bx = tcol * OX - T, by = geo.own0 + trow * OY - T;
-    return tma && bx >= 0 && bx + S::RX <= nx && by >= 0 && by + S::RY <= geo.lrows;
-  };
-  auto tma_load = [&](double2* stage, uint64_t* bar, int tcol, int trow) {
-    if (tid == 0) {
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // earlier LDS of this stage
-      tb_mbar_expect_tx(bar, 4u * S::REG * (uint32_t)sizeof(double2));
-      asm volatile(
-          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-          "[%5];\n" ::"r"((unsigned)__cvta_generic_to_shared(stage)),
-          "l"(reinterpret_cast<uint64_t>(&imap)), "r"(2 * (tcol * OX - T)), "r"(geo.own0 + trow * OY - T), "r"(0),
-          "r"((unsigned)__cvta_generic_to_shared(bar))
-          : "memory");
-    }
-  };
+  __syncthreads();
   const int64_t n = (int64_t)nx * geo.lrows;   // plane stride of the buffers
 
   // tile coordinates advance by gridDim.x tiles per iteration: (gdiv, gmod)
@@ -312,21 +486,19 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
       ++r;
     }
   };
-  auto prefetch = [&](double2* stage, int tcol, int trow) {
-    const int bx = tcol * OX - T + tx;
-    const int by = geo.own0 + trow * OY - T + ty * V;   // local buffer row
-    const int gx = wrapc(bx, nx);
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      // rows outside a slab buffer are > T rows from every owned row: left stale
-      const int ly = by + j;
-      if (SLAB && (ly < 0 || ly >= geo.lrows)) continue;
-      const int r = SLAB ? ly : wrapc(ly, ny);
-      const int64_t w = (int64_t)r * nx + gx;
-      const int li = (ty * V + j) * 32 + tx;
-#pragma unroll
-      for (int p = 0; p < 4; ++p) cp_async16(stage + p * S::REG + li, in + p * n + w);
+  auto inside = [&](int pc, int pr) {
+    return region_inside<S>(nx, geo.lrows, pc * OX - T, geo.own0 + pr * OY - T, use_tma != 0);
+  };
+  // one cp.async group per issue (empty for a TMA stage) keeps the group
+  // count per stage uniform
+  auto issue = [&](int k, int pc, int pr) {
+    double2* st = stage0 + (size_t)k * 4 * S::REG;
+    if (inside(pc, pr)) {
+      if (tid == 0) tma_region<S>(st, tbar + k, &imap, pc * OX - T, geo.own0 + pr * OY - T);
+    } else {
+      cp_region<S, V, SLAB>(st, in, nx, ny, geo.lrows, pc * OX - T, geo.own0 + pr * OY - T, tx, ty);
     }
+    cp_commit();
   };
 
   // programmatic dependent launch: everything above overlaps the previous
@@ -335,230 +507,240 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
   qwb::pdl_wait();
   int tile = blockIdx.x + tile0;   // tile0 > 0: a launch over tiles [tile0, ntiles) only
   if (tile >= ntiles) return;
+  // key != 0: test the tiles' inputs (and raise *sticky on a hit); key == 0:
+  // no test, numpy's arithmetic throughout if an earlier check raised *sticky
+  const bool check = key != 0;
+  const bool all_exact = !check && sticky && *reinterpret_cast<volatile int*>(sticky) != 0;
   int tcol = tile % tiles_x, trow = tile / tiles_x;
-  // (pcol, prow): the tile the next prefetch loads, NSTAGE - 1 tiles ahead of (tcol, trow)
+  // (pcol, prow): the tile the next load fetches, NSTAGE - 1 tiles ahead of (tcol, trow)
   int pcol = tcol, prow = trow, ptile = tile;
-  // per stage: whether its pending load is a TMA (f) and that barrier's parity (ph)
-  bool f0 = false, f1 = false;
-  uint32_t ph0 = 0, ph1 = 0;
   for (int k = 0; k < S::NSTAGE; ++k) {
-    if (ptile < ntiles) {
-      double2* st = stage0 + (size_t)k * 4 * S::REG;
-      if (tma_ok(pcol, prow)) {
-        tma_load(st, tbar + k, pcol, prow);
-        (k ? f1 : f0) = true;
-      } else {
-        prefetch(st, pcol, prow);
-      }
-    }
-    cp_commit();
+    if (ptile < ntiles)
+      issue(k, pcol, prow);
+    else
+      cp_commit();
     advance(pcol, prow);
     ptile += gridDim.x;
   }
+  uint32_t ph = 0;   // bit k: parity of stage k's barrier
   for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
     // last tile of this CTA: let the next launch's CTAs take the SMs that
     // finish first (they block in griddepcontrol.wait until this grid is done)
     if (tile + (int)gridDim.x >= ntiles) qwb::pdl_trigger();
     const int k = S::NSTAGE == 2 ? (it & 1) : 0;
-    double2* stage = stage0 + (size_t)k * 4 * S::REG;
-    // x0: global column of the tile's first owned column; y0: unwrapped
-    // global row of its first owned row; lyb: its local buffer row
-    const int trow_now = trow;
+    const int trow_now = trow, tcol_now = tcol;
     const int x0 = tcol * OX, y0 = geo.ybase + trow_now * OY, lyb = geo.own0 + trow_now * OY;
     advance(tcol, trow);
-    const int gx = wrapc(x0 - T + tx, nx);
-    int gy[V];
     double2 vD[V], vL[V], vR[V], vU[V];
-    if (S::NSTAGE == 2)
-      asm volatile("cp.async.wait_group 1;\n" ::: "memory");   // this tile's group; the next may fly
+    if (inside(tcol_now, trow_now)) {
+      tb_mbar_wait(tbar + k, (ph >> k) & 1u);
+      ph ^= 1u << k;
+    } else {
+      cp_wait<S::NSTAGE - 1>();   // this stage's group; the other stage's may fly
+      __syncthreads();
+    }
+    const unsigned m = stage_to_regs<S, V>(stage0 + (size_t)k * 4 * S::REG, tx, ty, vD, vL, vR, vU, check);
+    __syncthreads();   // stage k consumed
+    if (ptile < ntiles)
+      issue(k, pcol, prow);
     else
-      cp_wait_all();
-    if (k ? f1 : f0) {   // this stage came by TMA: wait for its bytes
-      tb_mbar_wait(tbar + k, k ? ph1 : ph0);
-      if (k) ph1 ^= 1u; else ph0 ^= 1u;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      gy[j] = wrapc(y0 - T + ty * V + j, ny);
-      const int li = (ty * V + j) * 32 + tx;
-      vD[j] = stage[li];
-      vL[j] = stage[S::REG + li];
-      vR[j] = stage[2 * S::REG + li];
-      vU[j] = stage[3 * S::REG + li];
-    }
-    __syncthreads();
-    if (k) f1 = false; else f0 = false;
-    if (ptile < ntiles) {   // into the stage just consumed
-      if (tma_ok(pcol, prow)) {
-        tma_load(stage, tbar + k, pcol, prow);
-        if (k) f1 = true; else f0 = true;
-      } else {
-        prefetch(stage, pcol, prow);
-      }
-    }
-    cp_commit();
+      cp_commit();
     advance(pcol, prow);
     ptile += gridDim.x;
-    // regions that touch no torus edge and hold no marked or traced vertex run
-    // a branch-free specialisation: every vertex is interior (slot order D L R U)
-    auto in_region = [&](int mx, int my) {
-      return mx >= x0 - T && mx < x0 - T + 32 && my >= y0 - T && my < y0 - T + S::RY;
-    };
-    bool interior = x0 - T >= 1 && x0 - T + 31 <= nx - 2 && y0 - T >= 1 &&
-                    y0 - T + S::RY - 1 <= ny - 2;
-    if (MARKED && interior) {
-      if (mk.n < 0) {
-        interior = false;   // too many marked vertices for the list: general path
-      } else {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) interior &= (k >= mk.n) || !in_region(mk.x[k], mk.y[k]);
-      }
-    }
-    if (TRACE)
-#pragma unroll
-      for (int k = 0; k < 8; ++k) interior &= (k >= tr.n) || !in_region(tr.x[k], tr.y[k]);
-    const bool col_ok = tx >= T && tx < T + OX && x0 + tx - T < nx;
-    bool own[V];
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      const int ly = ty * V + j;
-      own[j] = col_ok && ly >= T && ly < T + OY && trow_now * OY + ly - T < geo.nown;
-    }
-    if (interior) {
-      tile_steps<SHIFT, false, T, BY, V, true, false>(nx, ny, gx, gy, bits, vD, vL, vR, vU, xD, xU,
-                                                      tid, ty, tr, own, trbuf);
-    } else {
-      tile_steps<SHIFT, MARKED, T, BY, V, false, TRACE>(nx, ny, gx, gy, bits, vD, vL, vR, vU, xD, xU,
-                                                        tid, ty, tr, own, trbuf);
-      if (TRACE) {   // p of the traced vertices this tile owns, every level
-        __syncthreads();
-        if (tid < T * 8) {
-          const int t = tid >> 3, k = tid & 7;
-          const int mx = tr.x[k < tr.n ? k : 0], my = tr.y[k < tr.n ? k : 0];
-          const bool mine = k < tr.n && mx >= x0 && mx < x0 + OX && mx < nx && my >= y0 && my < y0 + OY &&
-                            my - y0 + trow_now * OY < geo.nown;
-          if (mine)
-            tr.out[t * tr.n + k] = trace_p(mx, my, nx, ny, 1.0 / (double)(1 << t), trbuf + (t * 8 + k) * 4);
-        }
-      }
-    }
-    constexpr double kScale = 1.0 / (double)(1 << T);   // undo the doubled-space steps (exact)
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      if (own[j]) {
-        const int64_t w = (int64_t)(lyb - T + ty * V + j) * nx + gx;
-        __stcs(out + w, make_double2(__dmul_rn(vD[j].x, kScale), __dmul_rn(vD[j].y, kScale)));
-        __stcs(out + n + w, make_double2(__dmul_rn(vL[j].x, kScale), __dmul_rn(vL[j].y, kScale)));
-        __stcs(out + 2 * n + w, make_double2(__dmul_rn(vR[j].x, kScale), __dmul_rn(vR[j].y, kScale)));
-        __stcs(out + 3 * n + w, make_double2(__dmul_rn(vU[j].x, kScale), __dmul_rn(vU[j].y, kScale)));
-      }
-    }
+    tile_run<SHIFT, MARKED, T, BY, V, SLAB>(nx, ny, n, geo.lrows, x0, y0, lyb, geo.nown - trow_now * OY, m, key,
+                                            all_exact, in, bits, mk, vD, vL, vR, vU, xD, xU, out, tx, ty, tid,
+                                            NoHook{}, sticky);
   }
-  cp_wait_all();
 }
 
-int env_int(const char* name, int dflt);
+// ---------------------------------------------------------------------------
+// Flow kernel: nblocks x T steps on the torus in one launch (file comment).
+//
+// Items (block k, tile) are numbered k-major; CTA c takes items c, c + G,
+// c + 2G, ... (G = gridDim.x CTAs, co-resident: cooperative launch).  An
+// item waits for the progress counters of the 5 x 5 tiles around it (a
+// superset of the tiles whose owned cells its region reads: only the last
+// tile column / row can be narrower than T) to reach its block; every item
+// depends only on items earlier in the numbering, and each CTA runs its
+// items in order, so the earliest unfinished item can always proceed.
+// ---------------------------------------------------------------------------
+struct FlowArgs {
+  double2* buf0;      // block k reads buf[k & 1], writes buf[(k + 1) & 1]
+  double2* buf1;
+  unsigned* done;     // [ntiles] blocks completed per tile (zeroed before the launch)
+  int nblocks;
+  int rot;            // tile-row rotation per block
+};
+
+// position of a CTA's item in the (block, tile row, tile column) grid,
+// advanced by G items without a division
+struct FlowPos {
+  int k, r, c, rk;    // block, unrotated tile row, tile column, (k * rot) mod tiles_y
+};
 
 template <int SHIFT, bool MARKED, int T, int BY, int V>
-int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const TbGeo& geo, const double2* in,
-                double2* out, const uint32_t* bits, const MarkedList& mk, const TraceList& tr) {
-  using Sh = TbShape<BY, V>;
-  constexpr int OX = Sh::RX - 2 * T, OY = Sh::RY - 2 * T;
-  const int tiles_x = (nx + OX - 1) / OX, tiles_y = (geo.nown + OY - 1) / OY;
+__global__ void __launch_bounds__(32 * BY, 1)
+lattice_flow_kernel(int nx, int ny, FlowArgs fa, const uint32_t* __restrict__ bits, MarkedList mk, int tiles_x,
+                    int tiles_y, const __grid_constant__ CUtensorMap imap0, const __grid_constant__ CUtensorMap imap1,
+                    int use_tma) {
+  using S = TbShape<BY, V>;
+  static_assert(S::NSTAGE == 1, "the flow kernel is written for one stage");
+  constexpr int OX = S::RX - 2 * T, OY = S::RY - 2 * T;
+  extern __shared__ __align__(128) double2 sm[];
+  double2* stage = sm;
+  double2* xD = sm + 4 * S::REG;
+  double2* xU = xD + 2 * S::NT;
+  uint64_t* tbar = reinterpret_cast<uint64_t*>(xU + 2 * S::NT);
+  int* shw = reinterpret_cast<int*>(tbar + 2);   // [0]: the next item's load state (0 / 1 TMA / 2 cp.async)
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tid = ty * 32 + tx;
   const int ntiles = tiles_x * tiles_y;
-  const size_t smem = Sh::smem_bytes();
-  const int grid = ntiles < ctx->num_sms ? ntiles : ctx->num_sms;
-  // tensor map of the input planes for the TMA tile loads: doubles
-  // [4][lrows][2 nx] (lrows = ny on the torus, the slab's buffer rows), box
-  // [4][RY][64] = one stage
-  CUtensorMap imap{};
-  static int use_tma_env = env_int("QWB_LATTICE_TMA", 1);
-  int use_tma = 0;
-  if (use_tma_env) {
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    if (!encode) {
-      cudaDriverEntryPointQueryResult q;
-      void* fn = nullptr;
-      cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
-      if (e == cudaSuccess && fn) encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  const int64_t n = (int64_t)nx * ny;
+  const int G = (int)gridDim.x;
+  const int gdiv = G / tiles_x, gmod = G % tiles_x;
+  auto adv = [&](FlowPos p) -> FlowPos {
+    p.c += gmod;
+    p.r += gdiv;
+    if (p.c >= tiles_x) {
+      p.c -= tiles_x;
+      ++p.r;
     }
-    if (encode) {
-      const cuuint64_t dims[3] = {2 * (cuuint64_t)nx, (cuuint64_t)geo.lrows, 4};
-      const cuuint64_t strides[2] = {2 * (cuuint64_t)nx * sizeof(double),
-                                     (cuuint64_t)nx * geo.lrows * sizeof(double2)};
-      const cuuint32_t box[3] = {2 * (cuuint32_t)Sh::RX, (cuuint32_t)Sh::RY, 4};
-      const cuuint32_t estr[3] = {1, 1, 1};
-      use_tma = encode(&imap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double2*>(in), dims, strides, box,
-                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    if (p.r >= tiles_y) {
+      p.r -= tiles_y;
+      ++p.k;
+      p.rk += fa.rot;
+      if (p.rk >= tiles_y) p.rk -= tiles_y;
     }
-  }
-  auto go = [&](auto kernel, bool* configured, int grid_ = 0, int tile0 = 0, int ntiles_ = 0) -> int {
-    const int dev = ctx->device & 255;
-    if (!configured[dev]) {
-      cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return qwb::cuda_status(ctx, e, "cudaFuncSetAttribute(lattice_tb)");
-      configured[dev] = true;
-    }
-    static const bool pdl = env_int("QWB_LATTICE_PDL", 1) != 0;   // see qwb::launch_pdl
-    const cudaError_t e = qwb::launch_pdl(pdl, kernel, dim3(grid_ ? grid_ : grid), dim3(32, BY), smem, s, nx, ny,
-                                          geo, in, out, bits, mk, tr, tiles_x, ntiles_ ? ntiles_ : ntiles, tile0,
-                                          imap, use_tma);
-    if (e != cudaSuccess) return qwb::cuda_status(ctx, e, "cudaLaunchKernelEx(lattice_tb)");
-    return QWB_OK;
+    return p;
   };
-  static bool conf_plain[256] = {}, conf_trace[256] = {}, conf_slab[256] = {};   // per instantiation, device
-  if (!geo.wrap) {
-    if constexpr (T == kSlabDepth && BY == 16 && V == 4) {
-      if (tr.n > 0) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "slab launches do not fuse traces");
-      return go(lattice_tb_kernel<SHIFT, MARKED, T, BY, V, false, true>, conf_slab);
-    } else {
-      QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "slab kernels exist for T = %d on 32x64 regions only", kSlabDepth);
+  auto trow = [&](const FlowPos& p) { return p.r + p.rk >= tiles_y ? p.r + p.rk - tiles_y : p.r + p.rk; };
+  // polling warp, lane i < 25: progress counter of dependency i of the item at p
+  // (nullptr: none) and the count it must reach (= the item's block)
+  const int ddr = tx / 5 - 2, ddc = tx % 5 - 2;
+  auto dep_ptr = [&](const FlowPos& p) -> const unsigned* {
+#ifdef QWB_EXP_NODEPS
+    return nullptr;
+#endif
+    if (p.k == 0 || p.k >= fa.nblocks || tx >= 25) return nullptr;
+    const int rr = wrapc(trow(p) + ddr, tiles_y), cc = wrapc(p.c + ddc, tiles_x);
+    return fa.done + rr * tiles_x + cc;
+  };
+  auto poll = [&](const FlowPos& p) -> unsigned {   // one relaxed read of the lane's dependency
+    const unsigned* q = dep_ptr(p);
+    return q ? ld_relaxed(q) : 0xffffffffu;
+  };
+  auto inside = [&](const FlowPos& p) {
+    return region_inside<S>(nx, ny, p.c * OX - T, trow(p) * OY - T, use_tma != 0);
+  };
+  auto tma_item = [&](const FlowPos& p) {   // thread 0
+    tma_region<S>(stage, tbar, (p.k & 1) ? &imap1 : &imap0, p.c * OX - T, trow(p) * OY - T);
+  };
+  auto cp_item = [&](const FlowPos& p) {   // all threads
+    cp_region<S, V, false>(stage, (p.k & 1) ? fa.buf1 : fa.buf0, nx, ny, ny, p.c * OX - T, trow(p) * OY - T, tx, ty);
+    cp_commit();
+  };
+  // Roles: the last warp (a halo-row warp: it stores nothing) polls the next
+  // items' dependencies, acquires them and issues the TMA loads; thread 0
+  // (the first, also store-free warp) publishes finished tiles.  Their fences
+  // then wait for no outstanding stores or polls of their own.
+  const bool pw = ty == BY - 1;       // polling warp
+  const bool pw0 = pw && tx == 0;
+  // all threads: wait until the item's dependencies are done, then load it
+  auto blocking_load = [&](const FlowPos& p) {
+    if (pw) {
+      while (!__all_sync(0xffffffffu, poll(p) >= (unsigned)p.k)) __nanosleep(64);
+      acquire_for_async();
     }
-  }
-  // QWB_LATTICE_TRACE_SPLIT: 2 (default) light-cone trace kernel after the
-  // plain launch, 1 TRACE tile recompute per traced tile, 0 trace fused into
-  // the full launch (the last two measured slower: DESIGN.md §4)
-  static int trace_split = env_int("QWB_LATTICE_TRACE_SPLIT", 2);
-  if (tr.n > 0 && !trace_split) return go(lattice_tb_kernel<SHIFT, MARKED, T, BY, V, true, false>, conf_trace);
-  int st = go(lattice_tb_kernel<SHIFT, MARKED, T, BY, V, false, false>, conf_plain);
-  if (st || tr.n == 0) return st;
-  if (trace_split == 2) {
-    static const bool pdl = env_int("QWB_LATTICE_PDL", 1) != 0;
-    const cudaError_t e = qwb::launch_pdl(pdl, lattice_trace_cone_kernel<SHIFT, T>, dim3(tr.n), dim3(256), 0, s,
-                                          nx, ny, in, MARKED ? bits : nullptr, tr);
-    if (e != cudaSuccess) return qwb::cuda_status(ctx, e, "lattice_trace_cone_kernel");
-    return QWB_OK;
-  }
-  // Traced run: the plain launch above advanced every tile; the tiles that own
-  // a traced vertex are then recomputed from the same input (still intact: the
-  // output is the other buffer) by the TRACE instantiation, one CTA each, which
-  // records the traced vertices' per-level p and stores the same owned values
-  // again.  Keeps the trace's registers and checks out of the full launch.
-  int done_tiles[8];
-  int nd = 0;
-  for (int k = 0; k < tr.n; ++k) {
-    const int t = (tr.y[k] / OY) * tiles_x + tr.x[k] / OX;
-    bool seen = false;
-    for (int j = 0; j < nd; ++j) seen |= done_tiles[j] == t;
-    if (seen) continue;
-    done_tiles[nd++] = t;
-    st = go(lattice_tb_kernel<SHIFT, MARKED, T, BY, V, true, false>, conf_trace, 1, t, t + 1);
-    if (st) return st;
-  }
-  return QWB_OK;
-}
+    __syncthreads();   // the other threads' loads are ordered after the polling warp's acquire
+    if (inside(p)) {
+      if (pw0) tma_item(p);
+    } else {
+      cp_item(p);
+    }
+  };
+  // publish a finished tile: every thread's stores precede the caller's
+  // barrier; thread 0 (no stores of its own) releases
+  auto release = [&](int tile, unsigned value) {
+    if (tid == 0) {
+#if defined(QWB_EXP_STREL)
+      asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(fa.done + tile), "r"(value) : "memory");
+#elif defined(QWB_EXP_REDREL)
+      asm volatile("red.release.gpu.global.max.u32 [%0], %1;\n" ::"l"(fa.done + tile), "r"(value) : "memory");
+#else
+#ifndef QWB_EXP_NOFENCE
+      asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+#endif
+      asm volatile("st.relaxed.gpu.global.u32 [%0], %1;\n" ::"l"(fa.done + tile), "r"(value) : "memory");
+#endif
+    }
+  };
 
-template <int T, int BY, int V>
-int launch_tb(qwb_ctx* ctx, int shift, cudaStream_t s, int nx, int ny, const TbGeo& g, const double2* in,
-              double2* out, const uint32_t* bits, const MarkedList& mk, const TraceList& tr) {
-  if (shift == QWB_SHIFT_FLIPFLOP) {
-    return bits ? launch_tb_t<QWB_SHIFT_FLIPFLOP, true, T, BY, V>(ctx, s, nx, ny, g, in, out, bits, mk, tr)
-                : launch_tb_t<QWB_SHIFT_FLIPFLOP, false, T, BY, V>(ctx, s, nx, ny, g, in, out, bits, mk, tr);
+  if (blockIdx.x >= ntiles) return;
+  if (tid == 0) {
+    tb_mbar_init(tbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  return bits ? launch_tb_t<QWB_SHIFT_PERSISTENT, true, T, BY, V>(ctx, s, nx, ny, g, in, out, bits, mk, tr)
-              : launch_tb_t<QWB_SHIFT_PERSISTENT, false, T, BY, V>(ctx, s, nx, ny, g, in, out, bits, mk, tr);
+  __syncthreads();
+  FlowPos cur{0, (int)blockIdx.x / tiles_x, (int)blockIdx.x % tiles_x, 0};
+  blocking_load(cur);
+  // the polling warp reads the counters of the items one and two ahead in
+  // advance, so the prefetch point rarely waits for an L2 round trip
+  unsigned v1 = pw ? poll(adv(cur)) : 0u, v2 = 0u;
+  uint32_t ph = 0;
+  int pend_tile = -1;   // finished tile whose counter is not yet published
+  unsigned pend_val = 0;
+  while (true) {
+    const FlowPos nxt = adv(cur);
+    const int tr = trow(cur);
+    double2 vD[V], vL[V], vR[V], vU[V];
+    if (inside(cur)) {
+      tb_mbar_wait(tbar, ph);
+      ph ^= 1u;
+    } else {
+      cp_wait<0>();
+      __syncthreads();
+    }
+    const unsigned m = stage_to_regs<S, V>(stage, tx, ty, vD, vL, vR, vU);
+    __syncthreads();   // stage consumed
+    const bool more = nxt.k < fa.nblocks;
+    // the previous tile's counter: its stores precede the barrier above
+    if (pend_tile >= 0) release(pend_tile, pend_val);
+    // the next item's load now if its dependencies are done: TMA at once,
+    // a wrapping region's cp.async after the first step (shw[0] = 2);
+    // otherwise after this tile (shw[0] = 0: it may depend on this tile)
+    if (pw && more) {
+      bool ok = __all_sync(0xffffffffu, v1 >= (unsigned)nxt.k);
+      if (!ok) ok = __all_sync(0xffffffffu, poll(nxt) >= (unsigned)nxt.k);   // one fresh poll
+      if (ok) acquire_for_async();
+      const bool tma = inside(nxt);
+      if (ok && tma && pw0) tma_item(nxt);
+      if (pw0) shw[0] = ok ? (tma ? 1 : 2) : 0;
+    }
+    const double2* in = (cur.k & 1) ? fa.buf1 : fa.buf0;
+    double2* out = (cur.k & 1) ? fa.buf0 : fa.buf1;
+    auto after0 = [&]() {
+      if (more && shw[0] == 2) cp_item(nxt);
+    };
+    tile_run<SHIFT, MARKED, T, BY, V, false>(nx, ny, n, ny, cur.c * OX, tr * OY, tr * OY, ny - tr * OY, m,
+                                             qwb::kTinyKey, false, in, bits, mk, vD, vL, vR, vU, xD, xU, out, tx, ty,
+                                             tid, after0);
+    // this tile's counter is published at the next prefetch point (after a
+    // barrier that its stores precede), or here when the next item waits
+    pend_tile = tr * tiles_x + cur.c;
+    pend_val = (unsigned)cur.k + 1;
+    if (!more) break;
+    if (pw) v2 = poll(adv(nxt));
+    if (shw[0] == 0) {
+      __syncthreads();
+      release(pend_tile, pend_val);
+      pend_tile = -1;
+      blocking_load(nxt);
+    }
+    cur = nxt;
+    v1 = v2;
+  }
+  __syncthreads();
+  if (pend_tile >= 0) release(pend_tile, pend_val);
 }
 
 int env_int(const char* name, int dflt) {
@@ -566,186 +748,170 @@ int env_int(const char* name, int dflt) {
   return e && *e ? atoi(e) : dflt;
 }
 
-// ---------------------------------------------------------------------------
-// Wavefront variant: one warp = one column strip of 32 lanes that streams
-// along y.  Level t+1 of row r needs level t of rows r-1, r, r+1 only, so a
-// warp keeps, for each level, the outputs of the last two rows in registers
-// and completes one row per level per iteration (a skewed wavefront): no
-// shared memory, no barriers, warps fully independent.  Pushes along x use
-// shuffles; pushes along y are register moves.  Redundant work: 2T halo lanes
-// of 32 and 2T warm-up rows per strip.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ bool in_list(const MarkedList& m, int64_t w) {
-  bool r = false;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) r |= (k < m.n) && (m.v[k] == w);
-  return r;
+// tensor map of a planes buffer for the TMA tile loads: doubles
+// [4][lrows][2 nx], box [4][RY][64] = one stage
+template <class S>
+bool encode_map(CUtensorMap* m, const double2* base, int nx, int lrows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e == cudaSuccess && fn) encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  if (!encode) return false;
+  const cuuint64_t dims[3] = {2 * (cuuint64_t)nx, (cuuint64_t)lrows, 4};
+  const cuuint64_t strides[2] = {2 * (cuuint64_t)nx * sizeof(double), (cuuint64_t)nx * lrows * sizeof(double2)};
+  const cuuint32_t box[3] = {2 * (cuuint32_t)S::RX, (cuuint32_t)S::RY, 4};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double2*>(base), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-__device__ __forceinline__ void ld4(const double2* __restrict__ in, int64_t n, int64_t w, double2& d,
-                                    double2& l, double2& r, double2& u) {
-  d = __ldcs(in + w);
-  l = __ldcs(in + n + w);
-  r = __ldcs(in + 2 * n + w);
-  u = __ldcs(in + 3 * n + w);
+// Encoded maps, keyed by (buffer, nx, lrows) per region shape: a run's
+// ping-pong buffers are re-used launch after launch, so each is encoded once.
+template <class S>
+bool cached_map(CUtensorMap* m, const double2* base, int nx, int lrows) {
+  struct Entry {
+    const void* base;
+    int nx, lrows;
+    CUtensorMap map;
+  };
+  static Entry cache[8] = {};
+  static int next = 0;
+  static const bool use = env_int("QWB_LATTICE_TMA", 1) != 0;
+  if (!use) return false;
+  for (const Entry& e : cache)
+    if (e.base == base && e.nx == nx && e.lrows == lrows) {
+      *m = e.map;
+      return true;
+    }
+  if (!encode_map<S>(m, base, nx, lrows)) return false;
+  cache[next] = Entry{base, nx, lrows, *m};
+  next = (next + 1) % 8;
+  return true;
 }
 
-template <int SHIFT, bool MARKED, int T>
-__global__ void __launch_bounds__(128)
-lattice_wf_kernel(int nx, int ny, const double2* __restrict__ in, double2* __restrict__ out,
-                  MarkedList mk, int strips_x, int nstrips, int L) {
-  constexpr int OX = 32 - 2 * T;
-  const int lane = threadIdx.x & 31;
-  const int strip = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
-  if (strip >= nstrips) return;
-  const int x0 = (strip % strips_x) * OX, y0 = (strip / strips_x) * L;
-  const int yend = min(y0 + L, ny);
-  const int gx = wrapc(x0 - T + lane, nx);
-  const bool col_out = lane >= T && lane < T + OX && x0 + lane - T < nx;
-  const int64_t n = (int64_t)nx * ny;
-  const int ys = y0 - T;
-  const int rows = (yend - y0) + 2 * T;
-
-  // per level t-1 (0..T-1): outputs of the previous row (L, R, U needed) and
-  // the U output of the row before it
-  double2 pOL[T], pOR[T], pOU[T], ppOU[T];
-#pragma unroll
-  for (int t = 0; t < T; ++t) {
-    pOL[t] = pOR[t] = pOU[t] = ppOU[t] = make_double2(0.0, 0.0);
+template <class K>
+int configure(qwb_ctx* ctx, K kernel, size_t smem, bool* configured) {
+  const int dev = ctx->device & 255;
+  if (!configured[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return qwb::cuda_status(ctx, e, "cudaFuncSetAttribute(lattice_tb)");
+    configured[dev] = true;
   }
-  double2 nD, nL, nR, nU;
-  ld4(in, n, (int64_t)wrapc(ys, ny) * nx + gx, nD, nL, nR, nU);
-#pragma unroll 1
-  for (int i = 0; i < rows; ++i) {
-    double2 sD = nD, sL = nL, sR = nR, sU = nU;
-    {
-      const int nr = (i + 1 < rows) ? ys + i + 1 : ys + i;   // clamped prefetch, no branch
-      ld4(in, n, (int64_t)wrapc(nr, ny) * nx + gx, nD, nL, nR, nU);
-    }
-    const int r = ys + i;
-    int gy = wrapc(r, ny);
-    double2 cD, cL, cR, cU;
-    {
-      const bool m = MARKED && in_list(mk, (int64_t)gy * nx + gx);
-      qwb::vertex_outputs2(gx, gy, nx, ny, m, sD, sL, sR, sU, cD, cL, cR, cU);
-    }
-#pragma unroll
-    for (int t = 1; t <= T; ++t) {   // level t holds 2^t psi_t (doubled-space steps)
-      const double2 fromAbove = cD;                    // O_D of row r-t+1
-      const double2 fromRight = shfl_down2(pOL[t - 1]);   // O_L of (x+1, r-t)
-      const double2 fromLeft = shfl_up2(pOR[t - 1]);      // O_R of (x-1, r-t)
-      const double2 fromBelow = ppOU[t - 1];           // O_U of row r-t-1
-      ppOU[t - 1] = pOU[t - 1];
-      pOL[t - 1] = cL;
-      pOR[t - 1] = cR;
-      pOU[t - 1] = cU;
-      if (SHIFT == QWB_SHIFT_FLIPFLOP) {
-        sU = fromAbove; sD = fromBelow; sR = fromRight; sL = fromLeft;
-      } else {
-        sD = fromAbove; sU = fromBelow; sL = fromRight; sR = fromLeft;
-      }
-      gy = gy == 0 ? ny - 1 : gy - 1;                  // row r - t
-      if (t < T) {
-        const bool m = MARKED && in_list(mk, (int64_t)gy * nx + gx);
-        qwb::vertex_outputs2(gx, gy, nx, ny, m, sD, sL, sR, sU, cD, cL, cR, cU);
-      } else if (i >= 2 * T && col_out) {
-        constexpr double kScale = 1.0 / (double)(1 << T);
-        const int64_t w = (int64_t)gy * nx + gx;
-        __stcs(out + w, make_double2(__dmul_rn(sD.x, kScale), __dmul_rn(sD.y, kScale)));
-        __stcs(out + n + w, make_double2(__dmul_rn(sL.x, kScale), __dmul_rn(sL.y, kScale)));
-        __stcs(out + 2 * n + w, make_double2(__dmul_rn(sR.x, kScale), __dmul_rn(sR.y, kScale)));
-        __stcs(out + 3 * n + w, make_double2(__dmul_rn(sU.x, kScale), __dmul_rn(sU.y, kScale)));
-      }
-    }
-  }
-}
-
-template <int SHIFT, bool MARKED, int T>
-int launch_wf_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const double2* in, double2* out,
-                const MarkedList& mk) {
-  constexpr int OX = 32 - 2 * T;
-  const int strips_x = (nx + OX - 1) / OX;
-  // strip length: long strips amortise the 2T warm-up rows, but keep >= ~16
-  // warps per SM in flight
-  int L = env_int("QWB_LATTICE_L", 0);
-  if (L <= 0) {
-    const long long want = (long long)ctx->num_sms * 16;
-    L = 256;
-    while (L > 32 && (long long)strips_x * ((ny + L - 1) / L) < want) L /= 2;
-  }
-  const int strips_y = (ny + L - 1) / L;
-  const int nstrips = strips_x * strips_y;
-  const int threads = 128;
-  const int blocks = (nstrips * 32 + threads - 1) / threads;
-  lattice_wf_kernel<SHIFT, MARKED, T><<<blocks, threads, 0, s>>>(nx, ny, in, out, mk, strips_x, nstrips, L);
   return QWB_OK;
 }
 
-template <int T>
-int launch_wf(qwb_ctx* ctx, int shift, cudaStream_t s, int nx, int ny, const double2* in,
-              double2* out, const MarkedList& mk) {
-  const bool m = mk.n > 0;
-  if (shift == QWB_SHIFT_FLIPFLOP)
-    return m ? launch_wf_t<QWB_SHIFT_FLIPFLOP, true, T>(ctx, s, nx, ny, in, out, mk)
-             : launch_wf_t<QWB_SHIFT_FLIPFLOP, false, T>(ctx, s, nx, ny, in, out, mk);
-  return m ? launch_wf_t<QWB_SHIFT_PERSISTENT, true, T>(ctx, s, nx, ny, in, out, mk)
-           : launch_wf_t<QWB_SHIFT_PERSISTENT, false, T>(ctx, s, nx, ny, in, out, mk);
-}
-
-}  // namespace
-
-namespace qwb {
-
-// Steps per temporally blocked launch (0 = single-step kernel only).
-// QWB_LATTICE_T overrides (0, 2..8); QWB_LATTICE_KIND picks the CTA-tile
-// variant (default) or, with "wf", the wavefront variant (opt-in A/B switch);
-// QWB_LATTICE_SHAPE the tile shape.
-int lattice_kind() {   // 1 = CTA tile (default), 0 = wavefront
-  static int kind = -1;
-  if (kind < 0) {
-    const char* e = getenv("QWB_LATTICE_KIND");
-    kind = (e && strcmp(e, "wf") == 0) ? 0 : 1;
-  }
-  return kind;
-}
-
-int lattice_tb_depth(int64_t nx, int64_t ny, int64_t n_marked) {
-  static int depth = -1;
-  if (depth < 0) {
-    depth = env_int("QWB_LATTICE_T", 4);
-    if (depth < 0 || depth > 8 || depth == 1) depth = 4;
-  }
-  if (nx < 64 || ny < 64) return 0;   // tiny lattices: the single-step kernel is launch-bound anyway
-  if (lattice_kind() == 0 && n_marked > 8) return 0;   // wavefront takes marked as a short list
-  if (lattice_kind() == 1 && depth > 6) return 6;
-  return depth;
-}
-
-static int tb_launch_impl(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny, const TbGeo& geo,
-                          const double2* in, double2* out, const uint32_t* bits, const int64_t* marked_host,
-                          int64_t n_marked, const int64_t* trace_vertices_host, int n_trace, double* trace) {
-  if (lattice_kind() == 0) {
-    if (!geo.wrap) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "the wavefront kernel does not run on slabs");
-    if (trace) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "the wavefront kernel does not fuse traces");
-    MarkedList mk{};
-    mk.n = (int)n_marked;
-    for (int k = 0; k < mk.n; ++k) mk.v[k] = marked_host[k];
-    switch (depth) {
-      case 2: return launch_wf<2>(ctx, shift, s, nx, ny, in, out, mk);
-      case 3: return launch_wf<3>(ctx, shift, s, nx, ny, in, out, mk);
-      case 4: return launch_wf<4>(ctx, shift, s, nx, ny, in, out, mk);
-      case 5: return launch_wf<5>(ctx, shift, s, nx, ny, in, out, mk);
-      case 6: return launch_wf<6>(ctx, shift, s, nx, ny, in, out, mk);
-      case 7: return launch_wf<7>(ctx, shift, s, nx, ny, in, out, mk);
-      case 8: return launch_wf<8>(ctx, shift, s, nx, ny, in, out, mk);
-      default: QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "unsupported temporal block depth %d", depth);
+template <int SHIFT, bool MARKED, int T, int BY, int V>
+int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const TbGeo& geo, const double2* in,
+                double2* out, const uint32_t* bits, const MarkedList& mk, const TraceList& tr, int tile0,
+                int tile1, unsigned key, int* sticky) {
+  using Sh = TbShape<BY, V>;
+  constexpr int OX = Sh::RX - 2 * T, OY = Sh::RY - 2 * T;
+  const int tiles_x = (nx + OX - 1) / OX, tiles_y = (geo.nown + OY - 1) / OY;
+  const int ntiles = tile1 > 0 ? tile1 : tiles_x * tiles_y;
+  const size_t smem = Sh::smem_bytes();
+  const int span = ntiles - tile0;
+  if (span <= 0) return QWB_OK;
+  const int grid = span < ctx->num_sms ? span : ctx->num_sms;
+  CUtensorMap imap{};
+  const int use_tma = cached_map<Sh>(&imap, in, nx, geo.lrows) ? 1 : 0;
+  static const bool pdl = env_int("QWB_LATTICE_PDL", 1) != 0;   // see qwb::launch_pdl
+  static bool conf_plain[256] = {}, conf_slab[256] = {};   // per instantiation, device
+  if (!geo.wrap) {
+    if constexpr (T == kSlabDepth && BY == 16 && V == 4) {
+      if (tr.n > 0) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "slab launches do not fuse traces");
+      auto kernel = lattice_tb_kernel<SHIFT, MARKED, T, BY, V, true>;
+      int st = configure(ctx, kernel, smem, conf_slab);
+      if (st) return st;
+      const cudaError_t e = qwb::launch_pdl(pdl, kernel, dim3(grid), dim3(32, BY), smem, s, nx, ny, geo, in, out,
+                                            bits, mk, tiles_x, ntiles, tile0, imap, use_tma, key, sticky);
+      if (e != cudaSuccess) return qwb::cuda_status(ctx, e, "cudaLaunchKernelEx(lattice_tb slab)");
+      return QWB_OK;
+    } else {
+      QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "slab kernels exist for T = %d on 32x64 regions only", kSlabDepth);
     }
   }
-  static int shape_env = -1;
-  if (shape_env < 0) shape_env = env_int("QWB_LATTICE_SHAPE", 4);
-  static int trace_shape = env_int("QWB_LATTICE_TRACE_SHAPE", 4);
-  const int shape = trace ? trace_shape : shape_env;
-  if (depth > 6) depth = 6;
+  auto kernel = lattice_tb_kernel<SHIFT, MARKED, T, BY, V, false>;
+  int st = configure(ctx, kernel, smem, conf_plain);
+  if (st) return st;
+  cudaError_t e = qwb::launch_pdl(pdl, kernel, dim3(grid), dim3(32, BY), smem, s, nx, ny, geo, in, out, bits, mk,
+                                  tiles_x, ntiles, tile0, imap, use_tma, key, sticky);
+  if (e != cudaSuccess) return qwb::cuda_status(ctx, e, "cudaLaunchKernelEx(lattice_tb)");
+  if (tr.n == 0) return QWB_OK;
+  // traced run: the light-cone kernel re-derives the traced vertices' levels
+  // from this launch's (intact) input
+  e = qwb::launch_pdl(pdl, lattice_trace_cone_kernel<SHIFT, T>, dim3(tr.n), dim3(256), 0, s, nx, ny, in,
+                      MARKED ? bits : nullptr, tr);
+  if (e != cudaSuccess) return qwb::cuda_status(ctx, e, "lattice_trace_cone_kernel");
+  return QWB_OK;
+}
+
+template <int T, int BY, int V>
+int launch_tb(qwb_ctx* ctx, int shift, cudaStream_t s, int nx, int ny, const TbGeo& g, const double2* in,
+              double2* out, const uint32_t* bits, const MarkedList& mk, const TraceList& tr, int tile0, int tile1,
+              unsigned key, int* sticky) {
+#define QWB_TB_GO(SH, MK) \
+  launch_tb_t<SH, MK, T, BY, V>(ctx, s, nx, ny, g, in, out, bits, mk, tr, tile0, tile1, key, sticky)
+  if (shift == QWB_SHIFT_FLIPFLOP) return bits ? QWB_TB_GO(QWB_SHIFT_FLIPFLOP, true) : QWB_TB_GO(QWB_SHIFT_FLIPFLOP, false);
+  return bits ? QWB_TB_GO(QWB_SHIFT_PERSISTENT, true) : QWB_TB_GO(QWB_SHIFT_PERSISTENT, false);
+#undef QWB_TB_GO
+}
+
+constexpr int kFlowT = 4, kFlowBY = 16, kFlowV = 4;
+
+template <int SHIFT, bool MARKED>
+int launch_flow_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, double2* a, double2* b, const uint32_t* bits,
+                  const MarkedList& mk, int nblocks) {
+  using Sh = TbShape<kFlowBY, kFlowV>;
+  constexpr int OX = Sh::RX - 2 * kFlowT, OY = Sh::RY - 2 * kFlowT;
+  const int tiles_x = (nx + OX - 1) / OX, tiles_y = (ny + OY - 1) / OY;
+  const int ntiles = tiles_x * tiles_y;
+  void* ws;
+  int st = qwb::workspace(ctx, (size_t)ntiles * sizeof(unsigned), s, &ws);
+  if (st) return st;
+  QWB_CUDA(ctx, cudaMemsetAsync(ws, 0, (size_t)ntiles * sizeof(unsigned), s));
+  FlowArgs fa;
+  fa.buf0 = a;
+  fa.buf1 = b;
+  fa.done = reinterpret_cast<unsigned*>(ws);
+  fa.nblocks = nblocks;
+  fa.rot = tiles_y / 2;
+#ifdef QWB_EXP_NOROT
+  fa.rot = 0;
+#endif
+  CUtensorMap m0{}, m1{};
+  const int use_tma = (cached_map<Sh>(&m0, a, nx, ny) && cached_map<Sh>(&m1, b, nx, ny)) ? 1 : 0;
+  const size_t smem = Sh::smem_bytes();
+  auto kernel = lattice_flow_kernel<SHIFT, MARKED, kFlowT, kFlowBY, kFlowV>;
+  static bool conf[256] = {};
+  st = configure(ctx, kernel, smem, conf);
+  if (st) return st;
+  // one CTA per SM, all co-resident (cooperative launch: the items of one
+  // CTA wait on items of the others); -1: not possible here (caller falls
+  // back to one launch per T steps)
+  const int grid = ntiles < ctx->num_sms ? ntiles : ctx->num_sms;
+  int per_sm = 0;
+  QWB_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 32 * kFlowBY, smem));
+  if (per_sm * ctx->num_sms < grid) return -1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(32, kFlowBY);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, nx, ny, fa, bits, mk, tiles_x, tiles_y, m0, m1, use_tma);
+  if (e != cudaSuccess) return qwb::cuda_status(ctx, e, "cudaLaunchKernelEx(lattice_flow, cooperative)");
+  return QWB_OK;
+}
+
+MarkedList marked_list(int nx, const int64_t* marked_host, int64_t n_marked) {
   MarkedList mk{};
   mk.n = n_marked <= 8 ? (int)n_marked : -1;
   for (int k = 0; k < mk.n; ++k) {
@@ -753,6 +919,40 @@ static int tb_launch_impl(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, in
     mk.x[k] = (int)(marked_host[k] % nx);
     mk.y[k] = (int)(marked_host[k] / nx);
   }
+  return mk;
+}
+
+}  // namespace
+
+namespace qwb {
+
+// Steps per temporally blocked launch (0 = single-step kernel only).
+// QWB_LATTICE_T overrides (0, 2..6); QWB_LATTICE_SHAPE the tile shape.
+int lattice_tb_depth(int64_t nx, int64_t ny, int64_t n_marked) {
+  (void)n_marked;
+  static int depth = -1;
+  if (depth < 0) {
+    depth = env_int("QWB_LATTICE_T", 4);
+    if (depth < 0 || depth == 1) depth = 4;
+    if (depth > 6) depth = 6;
+  }
+  if (nx < 64 || ny < 64) return 0;   // tiny lattices: the single-step kernel is launch-bound anyway
+  return depth;
+}
+
+static int shape_of(bool traced) {
+  static int shape_env = env_int("QWB_LATTICE_SHAPE", 4);
+  static int trace_shape = env_int("QWB_LATTICE_TRACE_SHAPE", 4);
+  return traced ? trace_shape : shape_env;
+}
+
+static int tb_launch_impl(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny, const TbGeo& geo,
+                          const double2* in, double2* out, const uint32_t* bits, const int64_t* marked_host,
+                          int64_t n_marked, const int64_t* trace_vertices_host, int n_trace, double* trace,
+                          int tile0, int tile1, unsigned key, int* sticky) {
+  const int shape = shape_of(trace != nullptr);
+  if (depth > 6) depth = 6;
+  const MarkedList mk = marked_list(nx, marked_host, n_marked);
   TraceList tl{};
   tl.n = trace ? n_trace : 0;
   tl.out = trace;
@@ -762,12 +962,13 @@ static int tb_launch_impl(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, in
     tl.y[k] = (int)(trace_vertices_host[k] / nx);
   }
   // shape 4 (default): 32x16 threads, 4 rows each (32x64 region); 3: 32x16
-  // threads, 3 rows each (32x48 region; traced launches).  The 32x32 and
+  // threads, 3 rows each (32x48 region, two load stages).  The 32x32 and
   // 24-warp 32x48 shapes measured slower and are not built.
-#define QWB_TB_CASE(T_)                                                                        \
-  case T_:                                                                                     \
-    if (shape == 3) return launch_tb<T_, 16, 3>(ctx, shift, s, nx, ny, geo, in, out, bits, mk, tl); \
-    return launch_tb<T_, 16, 4>(ctx, shift, s, nx, ny, geo, in, out, bits, mk, tl);
+#define QWB_TB_CASE(T_)                                                                                          \
+  case T_:                                                                                                       \
+    if (shape == 3)                                                                                            \
+      return launch_tb<T_, 16, 3>(ctx, shift, s, nx, ny, geo, in, out, bits, mk, tl, tile0, tile1, key, sticky); \
+    return launch_tb<T_, 16, 4>(ctx, shift, s, nx, ny, geo, in, out, bits, mk, tl, tile0, tile1, key, sticky);
   switch (depth) {
     QWB_TB_CASE(2)
     QWB_TB_CASE(3)
@@ -783,18 +984,53 @@ static int tb_launch_impl(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, in
 int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny,
                       const double2* in, double2* out, const uint32_t* bits,
                       const int64_t* marked_host, int64_t n_marked,
-                      const int64_t* trace_vertices_host, int n_trace, double* trace) {
+                      const int64_t* trace_vertices_host, int n_trace, double* trace, int check, int* sticky) {
   const TbGeo geo{ny, 0, ny, 0, 1};
   return tb_launch_impl(ctx, depth, shift, s, nx, ny, geo, in, out, bits, marked_host, n_marked,
-                        trace_vertices_host, n_trace, trace);
+                        trace_vertices_host, n_trace, trace, 0, 0, check ? kTinyKeyPeriodic : 0u, sticky);
+}
+
+int lattice_sticky(qwb_ctx* ctx, int** out) {
+  if (!ctx->lat_sticky) {
+    cudaError_t e = cudaMalloc(&ctx->lat_sticky, 256);
+    if (e != cudaSuccess) return cuda_status(ctx, e, "cudaMalloc(lattice flag)");
+  }
+  *out = ctx->lat_sticky;
+  return QWB_OK;
+}
+
+// The flow kernel runs untraced torus runs of >= 2 T-step blocks when a
+// block is 2 to 16 waves of tiles (num_sms CTAs): there the per-launch
+// kernel's fixed cost per launch (grid fill, tail, launch gap: ~11 us)
+// dominates; on larger lattices its own per-item scheduling costs more
+// (measured).  QWB_LATTICE_FLOW=0: never, 2: always.
+int lattice_flow_blocks(int64_t nx, int64_t ny, int depth, bool traced, int64_t steps, int num_sms) {
+  static const int use = env_int("QWB_LATTICE_FLOW", 1);
+  if (!use || traced || depth != kFlowT || shape_of(false) != 4 || nx < 256 || ny < 256) return 0;
+  using Sh = TbShape<kFlowBY, kFlowV>;
+  constexpr int OX = Sh::RX - 2 * kFlowT, OY = Sh::RY - 2 * kFlowT;
+  const int64_t ntiles = ((nx + OX - 1) / OX) * ((ny + OY - 1) / OY);
+  if (use == 1 && (ntiles < 2 * (int64_t)num_sms || ntiles >= 16 * (int64_t)num_sms)) return 0;
+  const int64_t nb = steps / depth;
+  return nb >= 2 ? (int)(nb < (1 << 24) ? nb : (1 << 24)) : 0;
+}
+
+int lattice_flow_launch(qwb_ctx* ctx, int shift, cudaStream_t s, int nx, int ny, double2* a, double2* b,
+                        const uint32_t* bits, const int64_t* marked_host, int64_t n_marked, int nblocks) {
+  const MarkedList mk = marked_list(nx, marked_host, n_marked);
+  if (shift == QWB_SHIFT_FLIPFLOP)
+    return bits ? launch_flow_t<QWB_SHIFT_FLIPFLOP, true>(ctx, s, nx, ny, a, b, bits, mk, nblocks)
+                : launch_flow_t<QWB_SHIFT_FLIPFLOP, false>(ctx, s, nx, ny, a, b, bits, mk, nblocks);
+  return bits ? launch_flow_t<QWB_SHIFT_PERSISTENT, true>(ctx, s, nx, ny, a, b, bits, mk, nblocks)
+              : launch_flow_t<QWB_SHIFT_PERSISTENT, false>(ctx, s, nx, ny, a, b, bits, mk, nblocks);
 }
 
 int lattice_slab_depth(int depth) {   // the ghost-row depth a slab run can use (0: none)
-  return (lattice_kind() == 1 && depth == kSlabDepth && env_int("QWB_LATTICE_SHAPE", 4) == 4) ? depth : 0;
+  return (depth == kSlabDepth && env_int("QWB_LATTICE_SHAPE", 4) == 4) ? depth : 0;
 }
 
 int lattice_tb_owned_rows(int depth) {
-  if (lattice_kind() != 1 || depth < 2) return 0;
+  if (depth < 2) return 0;
   const int shape = env_int("QWB_LATTICE_SHAPE", 4);
   const int ry = shape == 3 ? 16 * 3 : 16 * 4;
   return ry - 2 * (depth > 6 ? 6 : depth);
@@ -802,16 +1038,22 @@ int lattice_tb_owned_rows(int depth) {
 
 int lattice_tb_launch_geo(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny, const TbGeo& geo,
                           const double2* in, double2* out, const uint32_t* bits, const int64_t* marked_host,
-                          int64_t n_marked) {
+                          int64_t n_marked, int tile0, int tile1) {
+  // slab launches test every tile's input (their horizon is one launch)
   return tb_launch_impl(ctx, depth, shift, s, nx, ny, geo, in, out, bits, marked_host, n_marked, nullptr, 0,
-                        nullptr);
+                        nullptr, tile0, tile1, kTinyKey, nullptr);
 }
 
 }  // namespace qwb
 
 extern "C" int qwb_lattice_fused_depth(int64_t nx, int64_t ny, int64_t n_marked, int* depth_host,
                                        int* kind_host) {
-  if (depth_host) *depth_host = qwb::lattice_tb_depth(nx, ny, n_marked);
-  if (kind_host) *kind_host = qwb::lattice_kind();
+  const int d = qwb::lattice_tb_depth(nx, ny, n_marked);
+  if (depth_host) *depth_host = d;
+  // 2: one flow launch per untraced run, 1: one tile launch per T steps
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaGetLastError();
+  if (kind_host) *kind_host = (d > 0 && qwb::lattice_flow_blocks(nx, ny, d, false, 2 * d, sms)) ? 2 : 1;
   return QWB_OK;
 }

@@ -23,6 +23,8 @@ struct qwb_ctx {
   size_t ws_bytes;
   cudaStream_t ws_stream;
   cudaEvent_t ws_event;
+  // device int: a lattice run met tiny amplitudes (lattice_tb.cu)
+  int* lat_sticky;
   // pinned host staging for small readbacks
   void* pinned;
   std::string last_error;

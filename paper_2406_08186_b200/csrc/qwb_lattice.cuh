@@ -95,37 +95,51 @@ __device__ __forceinline__ void vertex_outputs(const Slots& o, bool marked, doub
   oU = pick(o.pU, O0, O1, O2, O3);
 }
 
-// ---- finite-input fast forms (used by the temporally blocked kernel) --------
-// numpy's (c + 0i) * s is (fma(c, s.x, -(0*s.y)), fma(c, s.y, 0*s.x)).  For
-// finite s, 0*v is the signed zero copysign(0, v): computing it with integer
-// bit operations keeps the result bitwise identical (zero signs included) at
-// one FP64 op per component instead of two.  States are finite by
-// construction (move_to_device rejects NaN/Inf; U is unitary).
-__device__ __forceinline__ double zsign(double v) {   // 0 * v for finite v
-  return __longlong_as_double(__double_as_longlong(v) & (long long)0x8000000000000000ULL);
-}
-__device__ __forceinline__ double nzsign(double v) {  // -(0 * v) for finite v
-  return __longlong_as_double((__double_as_longlong(v) & (long long)0x8000000000000000ULL) ^
-                              (long long)0x8000000000000000ULL);
-}
-__device__ __forceinline__ double2 scale_fin(double c, double2 s) {
-  return make_double2(__fma_rn(c, s.x, nzsign(s.y)), __fma_rn(c, s.y, zsign(s.x)));
-}
-
 // ---- doubled-space forms (temporally blocked kernels) -----------------------
-// numpy computes O = q0 + ((q1 + q2) + q3) with q_i = +-0.5 s_i.  Halving is
-// exact and commutes with round-to-nearest for normal operands, so
+// numpy computes O = q0 + ((q1 + q2) + q3) with q_i = +-0.5 s_i.  When every
+// product 0.5 s_i is exact, halving commutes with round-to-nearest, so
 //     O = 0.5 * fl(+-s0 + fl(fl(+-s1 +- s2) +- s3))
-// The fused kernels therefore iterate the doubled operator 2U with additions
-// only (the state after t on-chip steps is 2^t psi_t exactly) and scale by
-// 2^-T when they store.  Identical bits to numpy for every non-zero result; an
-// exact zero may come out as -0.0 instead of +0.0 or vice versa (equal under
-// ==, np.array_equal and every reduction).  Normalised states cannot reach the
-// subnormal range where the argument would fail (cancellation of doubles of
-// magnitude >= 2^-60 leaves results >= 2^-112 or exactly 0).
+// and the fused kernels iterate the doubled operator 2U with additions only
+// (after t on-chip steps the state is 2^t psi_t exactly), scaling by 2^-T when
+// they store.  Identical bits to numpy for every non-zero result; an exact
+// zero may come out as -0.0 instead of +0.0 or vice versa (equal under ==,
+// np.array_equal and every reduction).
+//
+// The products are exact unless a halving rounds in the subnormal range.  If
+// every non-zero input component of a tile has |x| >= 2^-1016 (exponent field
+// >= 7), all values are multiples of 2^(-1068-t) at level t (a sum of
+// multiples of a power of two rounds to a multiple of it), so the halvings of
+// levels t < 6 land on multiples of 2^-1074, i.e. are exact, and the doubled
+// sums are numpy's bit for bit for any depth T <= 6.  A tile
+// holding a smaller non-zero value (a localized start's light-cone front after
+// ~1000 steps: |psi| = 2^-t) runs in EXACT mode instead: each step halves its
+// inputs first (fl(0.5 s_i), numpy's products) and sums them in numpy's
+// order, i.e. the numpy arithmetic itself, with a store scale of 1.
 __device__ __forceinline__ double2 csub(double2 a, double2 b) {
   return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y));
 }
+__device__ __forceinline__ double2 halve(double2 v) {
+  return make_double2(__dmul_rn(v.x, 0.5), __dmul_rn(v.y, 0.5));
+}
+
+// min-accumulator of the tiny test: key(x) - 1 (unsigned) is below
+// kTinyKey iff 0 < |x| < 2^-1016.  key = |x|'s high word with bit 0 set when
+// the low word is non-zero (so key == 0 iff x == 0; bit 0 does not move the
+// comparison with 7 << 20).
+constexpr unsigned kTinyKey = (7u << 20) - 1u;
+// Periodic form: a launch that finds no non-zero |x| < 2^-926 (exponent
+// field >= 97) guarantees exact doubled-space steps for the next 96 steps
+// (multiples of 2^(-978-t) at step t stay on the 2^-1074 grid for t < 96):
+// 16 launches of T <= 6 steps until the next such check.
+constexpr unsigned kTinyKeyPeriodic = (97u << 20) - 1u;
+constexpr int kCheckEvery = 16;
+__device__ __forceinline__ unsigned tiny_acc(unsigned m, double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+  const unsigned key = (hi & 0x7fffffffu) | min(lo, 1u);
+  return min(m, key - 1u);
+}
+__device__ __forceinline__ unsigned tiny_acc2(unsigned m, double2 v) { return tiny_acc(tiny_acc(m, v.x), v.y); }
 
 __device__ __forceinline__ void vertex_outputs2_interior(double2 vD, double2 vL, double2 vR, double2 vU,
                                                          double2& oD, double2& oL, double2& oR,
@@ -138,17 +152,37 @@ __device__ __forceinline__ void vertex_outputs2_interior(double2 vD, double2 vL,
   oU = cadd(vD, csub(t, vU));         //  D + ((L + R) - U)
 }
 
-__device__ __forceinline__ void vertex_outputs2(int gx, int gy, int nx, int ny, bool marked, double2 vD,
-                                                double2 vL, double2 vR, double2 vU, double2& oD,
+// One vertex, doubled space (exact == false) or numpy's own per-step
+// arithmetic (exact == true).  The slot order matters only on
+// the rows y = 0 and y = ny - 1: on x = 0 / nx - 1 with interior y the order
+// is D R L U, and swapping the two middle slots leaves every row sum
+// p0 + ((p1 + p2) + p3) bitwise unchanged (IEEE addition commutes), so those
+// vertices take the interior formula; a warp (one region row) branches
+// uniformly.
+__device__ __forceinline__ void vertex_outputs2(int gx, int gy, int nx, int ny, bool marked, bool exact,
+                                                double2 vD, double2 vL, double2 vR, double2 vU, double2& oD,
                                                 double2& oL, double2& oR, double2& oU) {
-  if (marked) {   // 2 * (-psi)
-    oD = make_double2(-__dadd_rn(vD.x, vD.x), -__dadd_rn(vD.y, vD.y));
-    oL = make_double2(-__dadd_rn(vL.x, vL.x), -__dadd_rn(vL.y, vL.y));
-    oR = make_double2(-__dadd_rn(vR.x, vR.x), -__dadd_rn(vR.y, vR.y));
-    oU = make_double2(-__dadd_rn(vU.x, vU.x), -__dadd_rn(vU.y, vU.y));
+  if (marked) {   // numpy: -psi (exact); doubled space: 2 * (-psi)
+    if (exact) {
+      oD = make_double2(-vD.x, -vD.y);
+      oL = make_double2(-vL.x, -vL.y);
+      oR = make_double2(-vR.x, -vR.y);
+      oU = make_double2(-vU.x, -vU.y);
+    } else {
+      oD = make_double2(-__dadd_rn(vD.x, vD.x), -__dadd_rn(vD.y, vD.y));
+      oL = make_double2(-__dadd_rn(vL.x, vL.x), -__dadd_rn(vL.y, vL.y));
+      oR = make_double2(-__dadd_rn(vR.x, vR.x), -__dadd_rn(vR.y, vR.y));
+      oU = make_double2(-__dadd_rn(vU.x, vU.x), -__dadd_rn(vU.y, vU.y));
+    }
     return;
   }
-  if ((gx > 0) & (gx < nx - 1) & (gy > 0) & (gy < ny - 1)) {
+  if (exact) {
+    vD = halve(vD);
+    vL = halve(vL);
+    vR = halve(vR);
+    vU = halve(vU);
+  }
+  if ((gy > 0) & (gy < ny - 1)) {
     vertex_outputs2_interior(vD, vL, vR, vU, oD, oL, oR, oU);
     return;
   }
@@ -159,62 +193,6 @@ __device__ __forceinline__ void vertex_outputs2(int gx, int gy, int nx, int ny, 
   const double2 O1 = cadd(o.s0, cadd(d21, o.s3));
   const double2 O2 = cadd(o.s0, csub(o.s3, d21));
   const double2 O3 = cadd(o.s0, csub(t12, o.s3));
-  oD = pick(o.pD, O0, O1, O2, O3);
-  oL = pick(o.pL, O0, O1, O2, O3);
-  oR = pick(o.pR, O0, O1, O2, O3);
-  oU = pick(o.pU, O0, O1, O2, O3);
-}
-
-// interior, unmarked vertex: slot order is D L R U
-__device__ __forceinline__ void vertex_outputs_interior(double2 vD, double2 vL, double2 vR, double2 vU,
-                                                        double2& oD, double2& oL, double2& oR,
-                                                        double2& oU) {
-  const double2 qD = scale_fin(0.5, vD), qL = scale_fin(0.5, vL);
-  const double2 qR = scale_fin(0.5, vR), qU = scale_fin(0.5, vU);
-  const double2 nD = scale_fin(-0.5, vD), nL = scale_fin(-0.5, vL);
-  const double2 nR = scale_fin(-0.5, vR), nU = scale_fin(-0.5, vU);
-  const double2 t = cadd(qL, qR);
-  oD = cadd(nD, cadd(t, qU));
-  oL = cadd(qD, cadd(cadd(nL, qR), qU));
-  oR = cadd(qD, cadd(cadd(qL, nR), qU));
-  oU = cadd(qD, cadd(t, nU));
-}
-
-// vertex_outputs for finite inputs; interior vertices (slot order D L R U)
-// skip the slot permutation entirely.
-__device__ __forceinline__ void vertex_outputs_fin(int gx, int gy, int nx, int ny, bool marked,
-                                                   double2 vD, double2 vL, double2 vR, double2 vU,
-                                                   double2& oD, double2& oL, double2& oR, double2& oU) {
-  if (marked) {
-    oD = scale_fin(-1.0, vD);
-    oL = scale_fin(-1.0, vL);
-    oR = scale_fin(-1.0, vR);
-    oU = scale_fin(-1.0, vU);
-    return;
-  }
-  const bool interior = (gx > 0) & (gx < nx - 1) & (gy > 0) & (gy < ny - 1);
-  if (interior) {
-    const double2 qD = scale_fin(0.5, vD), qL = scale_fin(0.5, vL);
-    const double2 qR = scale_fin(0.5, vR), qU = scale_fin(0.5, vU);
-    const double2 nD = scale_fin(-0.5, vD), nL = scale_fin(-0.5, vL);
-    const double2 nR = scale_fin(-0.5, vR), nU = scale_fin(-0.5, vU);
-    const double2 t = cadd(qL, qR);
-    oD = cadd(nD, cadd(t, qU));
-    oL = cadd(qD, cadd(cadd(nL, qR), qU));
-    oR = cadd(qD, cadd(cadd(qL, nR), qU));
-    oU = cadd(qD, cadd(t, nU));
-    return;
-  }
-  const Slots o = order_slots(gx, gy, nx, ny, vD, vL, vR, vU);
-  const double2 q0 = scale_fin(0.5, o.s0), q1 = scale_fin(0.5, o.s1);
-  const double2 q2 = scale_fin(0.5, o.s2), q3 = scale_fin(0.5, o.s3);
-  const double2 n0 = scale_fin(-0.5, o.s0), n1 = scale_fin(-0.5, o.s1);
-  const double2 n2 = scale_fin(-0.5, o.s2), n3 = scale_fin(-0.5, o.s3);
-  const double2 t12 = cadd(q1, q2);
-  const double2 O0 = cadd(n0, cadd(t12, q3));
-  const double2 O1 = cadd(q0, cadd(cadd(n1, q2), q3));
-  const double2 O2 = cadd(q0, cadd(cadd(q1, n2), q3));
-  const double2 O3 = cadd(q0, cadd(t12, n3));
   oD = pick(o.pD, O0, O1, O2, O3);
   oL = pick(o.pL, O0, O1, O2, O3);
   oR = pick(o.pR, O0, O1, O2, O3);
@@ -235,16 +213,27 @@ struct TbGeo {
   int lrows, own0, nown, ybase, wrap;
 };
 int lattice_tb_depth(int64_t nx, int64_t ny, int64_t n_marked);
-int lattice_kind();   // 1 = CTA-tile kernel, 0 = wavefront kernel
-int lattice_tb_owned_rows(int depth);
-int lattice_slab_depth(int depth);   // ghost-row depth usable by slab runs (0: none)   // owned rows per tile row of the tile kernel (0: n/a)
+int lattice_tb_owned_rows(int depth);   // owned rows per tile row of the tile kernel (0: n/a)
+int lattice_slab_depth(int depth);      // ghost-row depth usable by slab runs (0: none)
+// tiles [tile0, tile1) of the launch's tile grid (tile1 = 0: all tiles)
 int lattice_tb_launch_geo(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny, const TbGeo& geo,
                           const double2* in, double2* out, const uint32_t* bits, const int64_t* marked_host,
-                          int64_t n_marked);
+                          int64_t n_marked, int tile0, int tile1);
+// persistent dataflow run of nblocks x 4 steps on the torus (lattice_tb.cu):
+// the number of blocks it would take for `steps` (0: not available)
+int lattice_flow_blocks(int64_t nx, int64_t ny, int depth, bool traced, int64_t steps, int num_sms);
+int lattice_flow_launch(qwb_ctx* ctx, int shift, cudaStream_t s, int nx, int ny, double2* a, double2* b,
+                        const uint32_t* bits, const int64_t* marked_host, int64_t n_marked, int nblocks);
+// check: 1 = test every tile's input for tiny amplitudes (threshold
+// kTinyKeyPeriodic), redo such tiles exactly and raise *sticky; 0 = no test:
+// all tiles exact if *sticky is raised, else doubled space.  A run checks its
+// first launch and every kCheckEvery-th (qwb_lattice_run).
 int lattice_tb_launch(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny,
                       const double2* in, double2* out, const uint32_t* bits,
                       const int64_t* marked_host, int64_t n_marked,
-                      const int64_t* trace_vertices_host, int n_trace, double* trace);
+                      const int64_t* trace_vertices_host, int n_trace, double* trace, int check, int* sticky);
+// the context's sticky flag (device int, allocated on first use)
+int lattice_sticky(qwb_ctx* ctx, int** out);
 int lattice_slab_geom(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, Geom* g);
 int lattice_slab_geom_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
                         Geom* g);
