@@ -222,10 +222,148 @@ def cpu_reference(nx: int, sample_steps: int, threads: int):
                       f"median step {statistics.median(times) * 1e3:.1f} ms, min {min(times) * 1e3:.1f} ms"}
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def load_reference():
+    """The stock reference package installed by `pip install --target
+    baseline/_ref`, or None.  Never /root/reference itself."""
+    if not os.path.isdir(os.path.join(REF_DIR, "qwalk")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import qwalk
+    if not os.path.abspath(qwalk.__file__).startswith(REF_DIR):
+        return None
+    return qwalk
+
+
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference(args):
+    """The reference's own CPU path, unmodified, through its public API
+    (baseline/_ref): coined.evolution_operator once (timed apart), then per
+    bench step exactly one iteration of coined.simulate's loop body
+    (coined.py:263-270): move_to_device(ComplexVector(psi)) + matvec_mul on the
+    parallel engine with all host threads.  Also reported: the serial engine
+    (median / min over 10 steps) and ctqw.evolve_state per Taylor term on
+    hypercube(20).  Falls back to the oracle port when baseline/_ref is absent."""
     rank, world, local = dist_env()
     if rank != 0:
         return 0
+    qw = load_reference()
+    if qw is None:
+        return run_reference_port(args)
+    from qwalk import backend as RB
+    from qwalk import coined as RC
+    from qwalk import ctqw as RQ
+    threads = os.cpu_count() or 1
+    nx = args.nx
+    t0 = time.perf_counter()
+    g = qw.graphs.grid(nx, nx)
+    spec = RC.CoinedSpec(g)
+    eng = RB.init_engine("parallel", threads)
+    u = RC.evolution_operator(eng, spec)
+    u_dev = RB.move_to_device(eng, u)
+    build_s = time.perf_counter() - t0
+    rng = np.random.default_rng(0)
+    cur = rng.normal(size=u.n_rows) + 1j * rng.normal(size=u.n_rows)
+    cur /= np.linalg.norm(cur)
+
+    def step(e, ud, x):   # coined.simulate's loop body (coined.py:268-269)
+        return RB.matvec_mul(e, RB.move_to_device(e, RB.ComplexVector(x)), ud).entries
+
+    for _ in range(args.warmup):
+        cur = step(eng, u_dev, cur)
+    times = []
+    for _ in range(args.steps):
+        a = time.perf_counter()
+        cur = step(eng, u_dev, cur)
+        times.append(time.perf_counter() - a)
+    el = sum(times)
+    value = u.n_rows * args.steps / el
+    RB.stop_engine(eng)
+    # serial engine, same operator
+    eser = RB.init_engine("serial")
+    us_dev = RB.move_to_device(eser, u)
+    cur = step(eser, us_dev, cur)
+    ser = []
+    for _ in range(10):
+        a = time.perf_counter()
+        cur = step(eser, us_dev, cur)
+        ser.append(time.perf_counter() - a)
+    RB.stop_engine(eser)
+    del u, u_dev, us_dev
+    # CTQW: evolve_state on hypercube(20), gamma 1/20, marked {0}, t = 0.5
+    # (one sub-step); terms counted by wrapping the module's matvec_mul
+    dim = 20
+    t1 = time.perf_counter()
+    hs = RQ.CtqwSpec(qw.graphs.hypercube(dim), 1.0 / dim, 1.0, frozenset({0}))
+    h = RQ.build_hamiltonian(hs)
+    hbuild_s = time.perf_counter() - t1
+    count = [0]
+    orig = RQ.matvec_mul
+
+    def counted(*a, **k):
+        count[0] += 1
+        return orig(*a, **k)
+    RQ.matvec_mul = counted
+    ectq = RB.init_engine("parallel", threads)
+    psi = qw.WalkState(qw.VertexBasis(1 << dim), np.full(1 << dim, 2.0 ** (-dim / 2), dtype=np.complex128))
+    a = time.perf_counter()
+    RQ.evolve_state(ectq, h, psi, 0.5)
+    ctqw_s = time.perf_counter() - a
+    RQ.matvec_mul = orig
+    RB.stop_engine(ectq)
+    cfg = {"workload": f"grid {nx}x{nx} torus flip-flop Grover (C2), stock reference coined step",
+           "arcs": int(g.num_arcs), "coined_steps_per_bench_step": 1,
+           "parallelism": f"reference 'parallel' engine, {threads} threads"}
+    sample = (f"reference qwalk {qw.__version__} from baseline/_ref: one coined.simulate loop iteration "
+              f"(move_to_device + matvec_mul) per bench step on grid {nx}x{nx}, parallel engine "
+              f"{threads} threads: median {statistics.median(times) * 1e3:.1f} ms, min {min(times) * 1e3:.1f} ms "
+              f"over {len(times)} steps; U built once in {build_s:.1f} s (excluded)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": cfg,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference": {
+            "package": os.path.relpath(os.path.dirname(qw.__file__), ROOT), "version": qw.__version__,
+            "cpu_model": _cpu_model(), "os_cpu_count": os.cpu_count(),
+            "operator_build_s": build_s,
+            "parallel_engine": {"threads": threads, "median_ms": statistics.median(times) * 1e3,
+                                "min_ms": min(times) * 1e3, "steps": len(times),
+                                "arc_updates_per_s": u_arcs_per_s(g.num_arcs, statistics.median(times))},
+            "serial_engine": {"median_ms": statistics.median(ser) * 1e3, "min_ms": min(ser) * 1e3,
+                              "steps": len(ser),
+                              "arc_updates_per_s": u_arcs_per_s(g.num_arcs, statistics.median(ser))},
+            "ctqw_hypercube20": {"call": "ctqw.evolve_state(parallel engine, H, uniform psi, t=0.5)",
+                                 "hamiltonian_build_s": hbuild_s, "terms": count[0], "seconds": ctqw_s,
+                                 "ms_per_term": ctqw_s / max(count[0], 1) * 1e3,
+                                 "vertex_term_updates_per_s": (1 << dim) * count[0] / ctqw_s},
+        },
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def u_arcs_per_s(arcs: int, seconds: float) -> float:
+    return arcs / seconds if seconds > 0 else 0.0
+
+
+def run_reference_port(args):
+    """Fallback without baseline/_ref: the oracle's numpy port of
+    backend._csr_rows with the reference's row-block pool."""
     threads = os.cpu_count() or 1
     nx = args.nx
     from oracle import qwalk_oracle as O
@@ -254,8 +392,8 @@ def run_reference(args):
         "config": {"workload": f"grid {nx}x{nx} torus flip-flop Grover (C2), reference CPU algorithm",
                    "arcs": u.n_rows, "coined_steps_per_bench_step": sample, "parallelism": f"{threads} threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{sample} coined steps per bench step of grid {nx}x{nx}; numpy CSR "
-                                   "matvec restating backend._csr_rows with the reference's row-block pool"},
+                         "sample": f"baseline/_ref missing: {sample} coined steps per bench step of grid {nx}x{nx}; "
+                                   "numpy CSR matvec restating backend._csr_rows with the reference's row-block pool"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
