@@ -360,8 +360,11 @@ namespace hcs {
 constexpr int LB = 10;                     // low bits per tile
 constexpr int TILE = 1 << LB;              // vertices per tile
 constexpr uint32_t CHUNK_BYTES = TILE * sizeof(double2);
-// NS ring stages + a double-buffered acc tile + barriers
-constexpr size_t smem_bytes(int ns) { return (size_t)(ns + 2) * CHUNK_BYTES + (2 * ns + 4) * sizeof(uint64_t); }
+// NS ring stages + a double-buffered acc tile + barriers + per acc slot the
+// tile's 32 marked-bitmap words
+constexpr size_t smem_bytes(int ns) {
+  return (size_t)(ns + 2) * CHUNK_BYTES + (2 * ns + 4) * sizeof(uint64_t) + 2 * 32 * sizeof(uint32_t);
+}
 }  // namespace hcs
 
 __device__ __forceinline__ uint32_t nctaid_x() {
@@ -486,8 +489,10 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
   uint64_t* empty = full + NS;
   uint64_t* afull = empty + NS;                                // [2]
   uint64_t* aempty = afull + 2;                                // [2]
+  // [2][32]: per acc slot, the tile's marked-bitmap words (bulk-copied with
+  // the acc tile)
+  uint32_t* awords = reinterpret_cast<uint32_t*>(aempty + 2);
   __shared__ double red[CONS / 32 + 2];
-  __shared__ uint32_t mwords[CONS / 32][TILE / CONS];   // consumers: the tile's bitmap words
   const int tid = threadIdx.x;
   const int dim = op.dim;
   const int nh = dim - LB;                            // high bits (global)
@@ -523,8 +528,8 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
       // ---------------- producer lanes: stream the partner tiles in row order
       constexpr unsigned pmask = (SPLIT == 32) ? 0xffffffffu : ((1u << SPLIT) - 1u);
       constexpr uint32_t part = CHUNK_BYTES / SPLIT;
-      auto issue = [&](uint64_t* fb, double2* dst, const double2* src) {
-        if (pl == 0) mbar_expect_tx(fb, CHUNK_BYTES);
+      auto issue = [&](uint64_t* fb, double2* dst, const double2* src, uint32_t extra) {
+        if (pl == 0) mbar_expect_tx(fb, CHUNK_BYTES + extra);
         __syncwarp(pmask);
         bulk_g2s(reinterpret_cast<char*>(dst) + pl * part, reinterpret_cast<const char*>(src) + pl * part,
                  part, fb);
@@ -533,10 +538,13 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
         const uint32_t Hl = (uint32_t)tile, H = hbase | Hl;
         const int hs = __popc(H);
-        {   // the tile's acc values, consumed in the epilogue
+        {   // the tile's acc values and (marked runs) its 32 bitmap words,
+            // consumed in the epilogue; both complete on the acc slot's barrier
           const int ab = ti & 1;
           mbar_wait(aempty + ab, ((ti >> 1) & 1) ^ 1);
-          issue(afull + ab, accbuf + (size_t)ab * TILE, acc_in + ((int64_t)Hl << LB));
+          issue(afull + ab, accbuf + (size_t)ab * TILE, acc_in + ((int64_t)Hl << LB), op.bits ? 128u : 0u);
+          if (op.bits && pl == 0)
+            bulk_g2s(awords + ab * 32, op.bits + ((vbase + (tile << LB)) >> 5), 128u, afull + ab);
         }
         uint32_t setm = H, clrm = (~H) & hmask;
         for (int c = 0; c <= nh; ++c) {
@@ -553,7 +561,7 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
                                             : op.remote[b - nh_loc] + ((int64_t)Hl << LB);
           const int s = it % NS;
           mbar_wait(empty + s, ((it / NS) & 1) ^ 1);
-          issue(full + s, ring + (size_t)s * TILE, src);
+          issue(full + s, ring + (size_t)s * TILE, src, 0u);
           ++it;
         }
       }
@@ -638,8 +646,11 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
           ac[0][j] = cadd(ac[0][j], e[j]);
         }
       };
-      auto fold_own = [&](const double2* ch, auto Rc) {   // positions hs .. hs + LB - 1
+      // FAST: every position of the segment is in the 4-accumulator main part
+      // (hs >= 1 and hs + LB - 2 < main_end): no per-position branch
+      auto fold_own = [&](const double2* ch, auto Rc, auto Fc) {   // positions hs .. hs + LB - 1
         constexpr int R = decltype(Rc)::value;           // hs & 3
+        constexpr bool FAST = decltype(Fc)::value;
         const char* cb = reinterpret_cast<const char*>(ch);
 #pragma unroll
         for (int q = 0; q < LB; ++q) {
@@ -648,6 +659,12 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
           for (int j = 0; j < VPT; ++j) {
             const uint32_t off = (q % 2 == 0) ? (offs[j][q / 2] & 0xffffu) : (offs[j][q / 2] >> 16);
             e[j] = scale_real_z(g, *reinterpret_cast<const double2*>(cb + off));
+          }
+          if (FAST) {
+            const int a = (R + q + 3) & 3;   // constant once the loop is unrolled
+#pragma unroll
+            for (int j = 0; j < VPT; ++j) ac[a][j] = cadd(ac[a][j], e[j]);
+            continue;
           }
           const int i = hs + q - 1;
           if (i < 0) {
@@ -662,20 +679,6 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
           }
         }
       };
-      // the tile's marked-bitmap words (one per warp and j: a warp's 32
-      // vertices share a word) are copied to shared memory by lane 0 with
-      // cp.async now and land while the stream is folded (a register load
-      // here was spilled, and the spill store waited for the load)
-      if (op.bits && lane == 0) {
-#pragma unroll
-        for (int j = 0; j < VPT; ++j) {
-          const int64_t v = ((int64_t)H << LB) + tid + j * CONS;   // global id
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(&mwords[tid >> 5][j])),
-                       "l"(op.bits + (v >> 5))
-                       : "memory");
-        }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-      }
       // one stage: wait for it, read and scale this thread's entries, release
       auto take = [&](double2 (&e)[VPT]) {
         mbar_wait_u32(full_u32 + 8 * s, ph);
@@ -687,6 +690,39 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
         if (++s == NS) {
           s = 0;
           ph ^= 1u;
+        }
+      };
+      // two consecutive stages with one release point: both waits, then both
+      // chunks' loads in flight together
+      auto take2 = [&](double2 (&e1)[VPT], double2 (&e2)[VPT]) {
+        const uint32_t s1 = s, p1 = ph;
+        if (++s == NS) {
+          s = 0;
+          ph ^= 1u;
+        }
+        const uint32_t s2 = s, p2 = ph;
+        if (++s == NS) {
+          s = 0;
+          ph ^= 1u;
+        }
+        mbar_wait_u32(full_u32 + 8 * s1, p1);
+        mbar_wait_u32(full_u32 + 8 * s2, p2);
+        const double2* c1 = ring + (size_t)s1 * TILE;
+        const double2* c2 = ring + (size_t)s2 * TILE;
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+          e1[j] = c1[tid + j * CONS];
+          e2[j] = c2[tid + j * CONS];
+        }
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+          e1[j] = scale_real_z(g, e1[j]);
+          e2[j] = scale_real_z(g, e2[j]);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive_u32(empty_u32 + 8 * s1);
+          mbar_arrive_u32(empty_u32 + 8 * s2);
         }
       };
       auto addto = [&](double2 (&acc)[VPT], const double2 (&e)[VPT]) {
@@ -702,12 +738,22 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
         addto(x0, e);
         c = 1;
       }
+      double2 f[VPT];
       for (; c + 4 <= hs; c += 4) {
+#ifdef QWB_EXP_NOTAKE2
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           take(e);
           addto(ac[u], e);
         }
+#else
+        take2(e, f);
+        addto(ac[0], e);
+        addto(ac[1], f);
+        take2(e, f);
+        addto(ac[2], e);
+        addto(ac[3], f);
+#endif
       }
 #pragma unroll
       for (int u = 0; u < 3; ++u)
@@ -719,11 +765,26 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
       {
         mbar_wait_u32(full_u32 + 8 * s, ph);
         const double2* ch = ring + (size_t)s * TILE;
-        switch (hs & 3) {
-          case 0: fold_own(ch, std::integral_constant<int, 0>{}); break;
-          case 1: fold_own(ch, std::integral_constant<int, 1>{}); break;
-          case 2: fold_own(ch, std::integral_constant<int, 2>{}); break;
-          default: fold_own(ch, std::integral_constant<int, 3>{}); break;
+        using Y = std::true_type;
+        using N = std::false_type;
+#ifdef QWB_EXP_NOFAST
+        if (false) {
+#else
+        if (hs >= 1 && hs + LB - 2 < main_end) {
+#endif
+          switch (hs & 3) {
+            case 0: fold_own(ch, std::integral_constant<int, 0>{}, Y{}); break;
+            case 1: fold_own(ch, std::integral_constant<int, 1>{}, Y{}); break;
+            case 2: fold_own(ch, std::integral_constant<int, 2>{}, Y{}); break;
+            default: fold_own(ch, std::integral_constant<int, 3>{}, Y{}); break;
+          }
+        } else {
+          switch (hs & 3) {
+            case 0: fold_own(ch, std::integral_constant<int, 0>{}, N{}); break;
+            case 1: fold_own(ch, std::integral_constant<int, 1>{}, N{}); break;
+            case 2: fold_own(ch, std::integral_constant<int, 2>{}, N{}); break;
+            default: fold_own(ch, std::integral_constant<int, 3>{}, N{}); break;
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive_u32(empty_u32 + 8 * s);
@@ -739,11 +800,20 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
         constexpr int R = decltype(Rc)::value;   // slot of partner hs
         int cc = hs;
         for (; cc + 4 <= cme; cc += 4) {
+#ifdef QWB_EXP_NOTAKE2
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             take(e);
             addto(ac[(R + u) & 3], e);
           }
+#else
+          take2(e, f);
+          addto(ac[R & 3], e);
+          addto(ac[(R + 1) & 3], f);
+          take2(e, f);
+          addto(ac[(R + 2) & 3], e);
+          addto(ac[(R + 3) & 3], f);
+#endif
         }
 #pragma unroll
         for (int u = 0; u < 3; ++u)
@@ -765,14 +835,10 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
       const int ab = ti & 1;
       mbar_wait(afull + ab, (ti >> 1) & 1);
       const double2* ach = accbuf + (size_t)ab * TILE;
-      if (op.bits) {
-        if (lane == 0) asm volatile("cp.async.wait_all;\n" ::: "memory");
-        __syncwarp();
-      }
 #pragma unroll
       for (int j = 0; j < VPT; ++j) {
         const int64_t v = ((int64_t)tile << LB) + tid + j * CONS;   // local index
-        const uint32_t mword = op.bits ? mwords[tid >> 5][j] : 0u;
+        const uint32_t mword = op.bits ? awords[ab * 32 + ((tid + j * CONS) >> 5)] : 0u;
         if ((mword >> (v & 31)) & 1u) continue;   // marked: the fix-up warp's
         const double2 r = (m == main_end) ? cadd(cadd(ac[0][j], ac[1][j]), cadd(ac[2][j], ac[3][j])) : ac[0][j];
         const double2 t = cmul_np(alpha, cadd(x0[j], r));
