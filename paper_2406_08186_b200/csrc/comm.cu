@@ -297,6 +297,16 @@ static int ghost_exchange_nccl(qwb_ctx* ctx, int64_t nx, int64_t nl, int64_t G, 
 // `steps` coined steps on a ghost-row slab: temporally blocked launches of
 // `ghost` steps each (ghost-row exchange before each), the remainder as
 // single pull steps (one-row exchange before each).  Result in a or b.
+//
+// The exchange overlaps the first launch after it: that launch is split by
+// tile rows into a middle band, whose regions read owned rows only, and two
+// edge bands.  The NCCL group runs on the comm stream while the middle band
+// runs on the caller's stream on all SMs but kSlabFreeSMs (so NCCL's kernels
+// find SMs: nothing waits on anything inside a kernel, so even without free
+// SMs the two only serialise); the edge bands follow after an event wait.
+// QWB_SLAB_OVERLAP=0: exchange in stream order before the launch instead.
+constexpr int kSlabFreeSMs = 8;
+
 int qwb_slab_run_fused(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
                        int shift, const uint32_t* marked_bits, const int64_t* marked_host, int64_t n_marked,
                        qwb_z* a, qwb_z* b, int64_t steps, int rank_below, int rank_above, int* final_in_b_host,
@@ -307,44 +317,84 @@ int qwb_slab_run_fused(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t
     QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "neighbour ranks out of range");
   if (steps < 0) QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "steps must be >= 0");
   cudaStream_t s = qwb::as_stream(stream);
+  cudaStream_t cs = ctx->comm_stream;
   double2* cur = reinterpret_cast<double2*>(a);
   double2* nxt = reinterpret_cast<double2*>(b);
-  // No in-kernel wait on the exchange: a persistent launch whose CTAs spin
-  // on a flag raised after an NCCL kernel on another stream deadlocks when
-  // NCCL needs more co-resident CTAs than the SMs the launch leaves free
-  // (seen at 8192 columns).  The exchange is 4 ghost rows per 4 steps, under
-  // 8 % of a launch's bytes, so it runs in stream order before the launch.
   // G = mT: per exchange of g = jT rows (j = m, fewer at the end), j launches
   // over the owned rows extended by (j-1)T, ..., T, 0 rows each side; the last
   // < T steps as single pull steps (1-row exchange)
   const int T = qwb::kSlabDepth;
   if (qwb::lattice_slab_depth(T) != T || ghost < T || ghost % T)
     QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "ghost rows must be a multiple of the slab depth");
+  if (n_marked > 0 && (!marked_bits || !marked_host))
+    QWB_FAIL(ctx, QWB_E_INVALID_ARGUMENT, "marked vertices need both the bitmap and the host list");
+  static const int overlap = qwb::env_flag("QWB_SLAB_OVERLAP", 1);
   int swaps = 0;
-  auto launch = [&](int nsteps, int ext) -> int {
-    const int st = qwb_slab_advance_local(ctx, nx, ny, y0, ny_local, ghost, shift, marked_bits, marked_host,
-                                          n_marked, reinterpret_cast<qwb_z*>(cur), reinterpret_cast<qwb_z*>(nxt),
-                                          nsteps, ext, stream);
+  auto swap = [&]() {
     double2* t = cur;
     cur = nxt;
     nxt = t;
     ++swaps;
+  };
+  auto launch = [&](int nsteps, int ext) -> int {
+    const int st = qwb_slab_advance_local(ctx, nx, ny, y0, ny_local, ghost, shift, marked_bits, marked_host,
+                                          n_marked, reinterpret_cast<qwb_z*>(cur), reinterpret_cast<qwb_z*>(nxt),
+                                          nsteps, ext, stream);
+    swap();
     return st;
+  };
+  // the T-step launch over owned rows + ext, as middle band (during the
+  // exchange) and edge bands (after it); false: no middle band here
+  auto overlapped = [&](int g, int ext, int* st) -> bool {
+    const qwb::TbGeo geo{(int)(ny_local + 2 * ghost), (int)ghost - ext, (int)ny_local + 2 * ext, (int)(y0 - ext), 0};
+    int tx, ty;
+    const int oy = qwb::lattice_tb_tiles(T, (int)nx, geo.nown, &tx, &ty);
+    // tile row r: local rows own0 + r oy + [-T, oy + T) must lie in the owned rows
+    const int r_lo = (ext + T + oy - 1) / oy;
+    const int r_hi_num = (int)ny_local + ext - T - oy;
+    const int r_hi = r_hi_num >= 0 ? r_hi_num / oy : -1;
+    if (!overlap || r_lo > r_hi || r_hi >= ty) return false;
+    *st = QWB_OK;
+    auto part = [&](int t0, int t1, int cap) -> int {
+      if (t1 <= t0) return QWB_OK;
+      return qwb::lattice_tb_launch_geo(ctx, T, shift, s, (int)nx, (int)ny, geo, cur, nxt, marked_bits, marked_host,
+                                        n_marked, t0, t1, cap);
+    };
+    cudaError_t e = cudaEventRecord(ctx->ev_ready, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ctx->ev_ready, 0);
+    if (e != cudaSuccess) {
+      *st = qwb::cuda_status(ctx, e, "slab exchange ordering");
+      return true;
+    }
+    *st = ghost_exchange_nccl(ctx, nx, ny_local, ghost, g, cur, rank_below, rank_above, cs);
+    if (!*st) *st = qwb::cuda_status_if(ctx, cudaEventRecord(ctx->ev_done, cs), "cudaEventRecord");
+    if (!*st) *st = part(r_lo * tx, (r_hi + 1) * tx, ctx->num_sms - kSlabFreeSMs);
+    if (!*st) *st = qwb::cuda_status_if(ctx, cudaStreamWaitEvent(s, ctx->ev_done, 0), "cudaStreamWaitEvent");
+    if (!*st) *st = part(0, r_lo * tx, 0);
+    if (!*st) *st = part((r_hi + 1) * tx, tx * ty, 0);
+    swap();
+    return true;
   };
   for (int64_t k = 0; k < steps;) {
     int64_t g = (steps - k) / T * T;
     if (g > ghost) g = ghost;
     if (g == 0) g = 1;
-    int st = ghost_exchange_nccl(ctx, nx, ny_local, ghost, (int)g, cur, rank_below, rank_above, s);
-    if (st) return st;
+    int st = QWB_OK;
     if (g == 1) {
-      st = launch(1, 0);
+      st = ghost_exchange_nccl(ctx, nx, ny_local, ghost, 1, cur, rank_below, rank_above, s);
+      if (!st) st = launch(1, 0);
     } else {
-      for (int ext = (int)g - T; ext >= 0 && !st; ext -= T) st = launch(T, ext);
+      int ext = (int)g - T;
+      if (!overlapped((int)g, ext, &st)) {
+        st = ghost_exchange_nccl(ctx, nx, ny_local, ghost, (int)g, cur, rank_below, rank_above, s);
+        if (!st) st = launch(T, ext);
+      }
+      for (ext -= T; ext >= 0 && !st; ext -= T) st = launch(T, ext);
     }
     if (st) return st;
     k += g;
   }
+  QWB_LAUNCH_CHECK(ctx, "slab launches");
   if (final_in_b_host) *final_in_b_host = swaps & 1;
   return QWB_OK;
 }

@@ -807,7 +807,7 @@ int configure(qwb_ctx* ctx, K kernel, size_t smem, bool* configured) {
 template <int SHIFT, bool MARKED, int T, int BY, int V>
 int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const TbGeo& geo, const double2* in,
                 double2* out, const uint32_t* bits, const MarkedList& mk, const TraceList& tr, int tile0,
-                int tile1, unsigned key, int* sticky) {
+                int tile1, unsigned key, int* sticky, int grid_cap) {
   using Sh = TbShape<BY, V>;
   constexpr int OX = Sh::RX - 2 * T, OY = Sh::RY - 2 * T;
   const int tiles_x = (nx + OX - 1) / OX, tiles_y = (geo.nown + OY - 1) / OY;
@@ -815,7 +815,8 @@ int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const TbGeo& geo, 
   const size_t smem = Sh::smem_bytes();
   const int span = ntiles - tile0;
   if (span <= 0) return QWB_OK;
-  const int grid = span < ctx->num_sms ? span : ctx->num_sms;
+  const int cap = grid_cap > 0 && grid_cap < ctx->num_sms ? grid_cap : ctx->num_sms;
+  const int grid = span < cap ? span : cap;
   CUtensorMap imap{};
   const int use_tma = cached_map<Sh>(&imap, in, nx, geo.lrows) ? 1 : 0;
   static const bool pdl = env_int("QWB_LATTICE_PDL", 1) != 0;   // see qwb::launch_pdl
@@ -852,9 +853,9 @@ int launch_tb_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, const TbGeo& geo, 
 template <int T, int BY, int V>
 int launch_tb(qwb_ctx* ctx, int shift, cudaStream_t s, int nx, int ny, const TbGeo& g, const double2* in,
               double2* out, const uint32_t* bits, const MarkedList& mk, const TraceList& tr, int tile0, int tile1,
-              unsigned key, int* sticky) {
+              unsigned key, int* sticky, int grid_cap) {
 #define QWB_TB_GO(SH, MK) \
-  launch_tb_t<SH, MK, T, BY, V>(ctx, s, nx, ny, g, in, out, bits, mk, tr, tile0, tile1, key, sticky)
+  launch_tb_t<SH, MK, T, BY, V>(ctx, s, nx, ny, g, in, out, bits, mk, tr, tile0, tile1, key, sticky, grid_cap)
   if (shift == QWB_SHIFT_FLIPFLOP) return bits ? QWB_TB_GO(QWB_SHIFT_FLIPFLOP, true) : QWB_TB_GO(QWB_SHIFT_FLIPFLOP, false);
   return bits ? QWB_TB_GO(QWB_SHIFT_PERSISTENT, true) : QWB_TB_GO(QWB_SHIFT_PERSISTENT, false);
 #undef QWB_TB_GO
@@ -949,7 +950,7 @@ static int shape_of(bool traced) {
 static int tb_launch_impl(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny, const TbGeo& geo,
                           const double2* in, double2* out, const uint32_t* bits, const int64_t* marked_host,
                           int64_t n_marked, const int64_t* trace_vertices_host, int n_trace, double* trace,
-                          int tile0, int tile1, unsigned key, int* sticky) {
+                          int tile0, int tile1, unsigned key, int* sticky, int grid_cap = 0) {
   const int shape = shape_of(trace != nullptr);
   if (depth > 6) depth = 6;
   const MarkedList mk = marked_list(nx, marked_host, n_marked);
@@ -967,8 +968,10 @@ static int tb_launch_impl(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, in
 #define QWB_TB_CASE(T_)                                                                                          \
   case T_:                                                                                                       \
     if (shape == 3)                                                                                            \
-      return launch_tb<T_, 16, 3>(ctx, shift, s, nx, ny, geo, in, out, bits, mk, tl, tile0, tile1, key, sticky); \
-    return launch_tb<T_, 16, 4>(ctx, shift, s, nx, ny, geo, in, out, bits, mk, tl, tile0, tile1, key, sticky);
+      return launch_tb<T_, 16, 3>(ctx, shift, s, nx, ny, geo, in, out, bits, mk, tl, tile0, tile1, key, sticky, \
+                                  grid_cap);                                                                 \
+    return launch_tb<T_, 16, 4>(ctx, shift, s, nx, ny, geo, in, out, bits, mk, tl, tile0, tile1, key, sticky,   \
+                                grid_cap);
   switch (depth) {
     QWB_TB_CASE(2)
     QWB_TB_CASE(3)
@@ -1038,10 +1041,20 @@ int lattice_tb_owned_rows(int depth) {
 
 int lattice_tb_launch_geo(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny, const TbGeo& geo,
                           const double2* in, double2* out, const uint32_t* bits, const int64_t* marked_host,
-                          int64_t n_marked, int tile0, int tile1) {
+                          int64_t n_marked, int tile0, int tile1, int grid_cap) {
   // slab launches test every tile's input (their horizon is one launch)
   return tb_launch_impl(ctx, depth, shift, s, nx, ny, geo, in, out, bits, marked_host, n_marked, nullptr, 0,
-                        nullptr, tile0, tile1, kTinyKey, nullptr);
+                        nullptr, tile0, tile1, kTinyKey, nullptr, grid_cap);
+}
+
+int lattice_tb_tiles(int depth, int nx, int nown, int* tiles_x, int* tiles_y) {
+  const int shape = env_int("QWB_LATTICE_SHAPE", 4);
+  const int ry = shape == 3 ? 16 * 3 : 16 * 4;
+  const int d = depth > 6 ? 6 : depth;
+  const int ox = 32 - 2 * d, oy = ry - 2 * d;
+  *tiles_x = (nx + ox - 1) / ox;
+  *tiles_y = (nown + oy - 1) / oy;
+  return oy;
 }
 
 }  // namespace qwb

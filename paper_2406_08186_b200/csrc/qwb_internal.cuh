@@ -39,6 +39,9 @@ namespace qwb {
 
 void set_error(qwb_ctx* ctx, const char* fmt, ...);
 int cuda_status(qwb_ctx* ctx, cudaError_t e, const char* what);
+inline int cuda_status_if(qwb_ctx* ctx, cudaError_t e, const char* what) {
+  return e == cudaSuccess ? 0 : cuda_status(ctx, e, what);
+}
 // scratch of at least `bytes` (256-B aligned), stream-ordered
 int workspace(qwb_ctx* ctx, size_t bytes, cudaStream_t s, void** out);
 int begin(qwb_ctx* ctx);   // checks ctx alive and sets the device

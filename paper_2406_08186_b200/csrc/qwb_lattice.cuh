@@ -215,10 +215,14 @@ struct TbGeo {
 int lattice_tb_depth(int64_t nx, int64_t ny, int64_t n_marked);
 int lattice_tb_owned_rows(int depth);   // owned rows per tile row of the tile kernel (0: n/a)
 int lattice_slab_depth(int depth);      // ghost-row depth usable by slab runs (0: none)
-// tiles [tile0, tile1) of the launch's tile grid (tile1 = 0: all tiles)
+// tiles [tile0, tile1) of the launch's tile grid (tile1 = 0: all tiles), on
+// at most grid_cap SMs (0: all)
 int lattice_tb_launch_geo(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny, const TbGeo& geo,
                           const double2* in, double2* out, const uint32_t* bits, const int64_t* marked_host,
-                          int64_t n_marked, int tile0, int tile1);
+                          int64_t n_marked, int tile0, int tile1, int grid_cap = 0);
+// the tile grid of a launch over nown owned rows (row-major tiles); returns
+// the owned rows per tile row
+int lattice_tb_tiles(int depth, int nx, int nown, int* tiles_x, int* tiles_y);
 // persistent dataflow run of nblocks x 4 steps on the torus (lattice_tb.cu):
 // the number of blocks it would take for `steps` (0: not available)
 int lattice_flow_blocks(int64_t nx, int64_t ny, int depth, bool traced, int64_t steps, int num_sms);
