@@ -75,19 +75,13 @@ __device__ __forceinline__ void tb_mbar_wait(uint64_t* b, uint32_t parity) {
 // progress counters of the flow kernel
 __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   unsigned v;
-#ifdef QWB_EXP_LDACQ
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-#else
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-#endif
   return v;
 }
 // after observing the counters with relaxed loads: acquire, then order the
 // async proxy (TMA / bulk copies) after it
 __device__ __forceinline__ void acquire_for_async() {
-#if !defined(QWB_EXP_NOFENCE) && !defined(QWB_EXP_LDACQ)
   asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
-#endif
   asm volatile("fence.proxy.async.global;\n" ::: "memory");
 }
 
@@ -348,13 +342,11 @@ __device__ __forceinline__ unsigned stage_to_regs(const double2* stage, int tx, 
     vL[j] = stage[S::REG + li];
     vR[j] = stage[2 * S::REG + li];
     vU[j] = stage[3 * S::REG + li];
-#ifndef QWB_EXP_NOCHECK
     if (!check) continue;
     m = qwb::tiny_acc2(m, vD[j]);
     m = qwb::tiny_acc2(m, vL[j]);
     m = qwb::tiny_acc2(m, vR[j]);
     m = qwb::tiny_acc2(m, vU[j]);
-#endif
   }
   return m;
 }
@@ -411,7 +403,6 @@ __device__ __forceinline__ void tile_run(int nx, int ny, int64_t n, int lrows, i
                     : tile_steps<SHIFT, MARKED, T, BY, V, false, false>(nx, ny, gx, gy, m, key, bits, vD, vL, vR, vU,
                                                                         xD, xU, tid, ty, after0);
   }
-#ifndef QWB_EXP_NOREDO
   if (tiny && !all_exact) {
     if (sticky && tid == 0) atomicOr(sticky, 1);
 #pragma unroll
@@ -432,7 +423,6 @@ __device__ __forceinline__ void tile_run(int nx, int ny, int64_t n, int lrows, i
       tile_steps<SHIFT, MARKED, T, BY, V, false, true>(nx, ny, gx, gy, 0u, 0u, bits, vD, vL, vR, vU, xD, xU, tid, ty,
                                                        NoHook{});
   }
-#endif
   const double sc = tiny ? 1.0 : 1.0 / (double)(1 << T);   // undo the doubled-space steps (exact)
   const bool col_ok = tx >= T && tx < T + OX && x0 + tx - T < nx;
 #pragma unroll
@@ -568,6 +558,7 @@ struct FlowArgs {
   double2* buf0;      // block k reads buf[k & 1], writes buf[(k + 1) & 1]
   double2* buf1;
   unsigned* done;     // [ntiles] blocks completed per tile (zeroed before the launch)
+  int* sticky;        // subnormal guard: a check block met tiny amplitudes (zeroed before the launch)
   int nblocks;
   int rot;            // tile-row rotation per block
 };
@@ -591,7 +582,9 @@ lattice_flow_kernel(int nx, int ny, FlowArgs fa, const uint32_t* __restrict__ bi
   double2* xD = sm + 4 * S::REG;
   double2* xU = xD + 2 * S::NT;
   uint64_t* tbar = reinterpret_cast<uint64_t*>(xU + 2 * S::NT);
-  int* shw = reinterpret_cast<int*>(tbar + 2);   // [0]: the next item's load state (0 / 1 TMA / 2 cp.async)
+  // [0]: the next item's load state (0 / 1 TMA / 2 cp.async); [2 + (it & 1)]:
+  // the run's sticky subnormal flag as seen by iteration it's item
+  int* shw = reinterpret_cast<int*>(tbar + 2);
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * 32 + tx;
   const int ntiles = tiles_x * tiles_y;
@@ -618,9 +611,6 @@ lattice_flow_kernel(int nx, int ny, FlowArgs fa, const uint32_t* __restrict__ bi
   // (nullptr: none) and the count it must reach (= the item's block)
   const int ddr = tx / 5 - 2, ddc = tx % 5 - 2;
   auto dep_ptr = [&](const FlowPos& p) -> const unsigned* {
-#ifdef QWB_EXP_NODEPS
-    return nullptr;
-#endif
     if (p.k == 0 || p.k >= fa.nblocks || tx >= 25) return nullptr;
     const int rr = wrapc(trow(p) + ddr, tiles_y), cc = wrapc(p.c + ddc, tiles_x);
     return fa.done + rr * tiles_x + cc;
@@ -629,6 +619,7 @@ lattice_flow_kernel(int nx, int ny, FlowArgs fa, const uint32_t* __restrict__ bi
     const unsigned* q = dep_ptr(p);
     return q ? ld_relaxed(q) : 0xffffffffu;
   };
+  auto need_of = [&](const FlowPos& p) -> unsigned { return (unsigned)p.k; };
   auto inside = [&](const FlowPos& p) {
     return region_inside<S>(nx, ny, p.c * OX - T, trow(p) * OY - T, use_tma != 0);
   };
@@ -646,10 +637,17 @@ lattice_flow_kernel(int nx, int ny, FlowArgs fa, const uint32_t* __restrict__ bi
   const bool pw = ty == BY - 1;       // polling warp
   const bool pw0 = pw && tx == 0;
   // all threads: wait until the item's dependencies are done, then load it
-  auto blocking_load = [&](const FlowPos& p) {
+  // after acquiring an item's dependencies: the sticky flag its block sees
+  // (any earlier check item of its dependency cone that met tiny amplitudes
+  // raised it before publishing its counter)
+  auto note_sticky = [&](int slot) {
+    if (pw0) shw[2 + slot] = *reinterpret_cast<volatile int*>(fa.sticky);
+  };
+  auto blocking_load = [&](const FlowPos& p, int slot) {
     if (pw) {
-      while (!__all_sync(0xffffffffu, poll(p) >= (unsigned)p.k)) __nanosleep(64);
+      while (!__all_sync(0xffffffffu, poll(p) >= need_of(p))) __nanosleep(64);
       acquire_for_async();
+      note_sticky(slot);
     }
     __syncthreads();   // the other threads' loads are ordered after the polling warp's acquire
     if (inside(p)) {
@@ -662,16 +660,8 @@ lattice_flow_kernel(int nx, int ny, FlowArgs fa, const uint32_t* __restrict__ bi
   // barrier; thread 0 (no stores of its own) releases
   auto release = [&](int tile, unsigned value) {
     if (tid == 0) {
-#if defined(QWB_EXP_STREL)
-      asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(fa.done + tile), "r"(value) : "memory");
-#elif defined(QWB_EXP_REDREL)
-      asm volatile("red.release.gpu.global.max.u32 [%0], %1;\n" ::"l"(fa.done + tile), "r"(value) : "memory");
-#else
-#ifndef QWB_EXP_NOFENCE
       asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
-#endif
       asm volatile("st.relaxed.gpu.global.u32 [%0], %1;\n" ::"l"(fa.done + tile), "r"(value) : "memory");
-#endif
     }
   };
 
@@ -682,7 +672,8 @@ lattice_flow_kernel(int nx, int ny, FlowArgs fa, const uint32_t* __restrict__ bi
   }
   __syncthreads();
   FlowPos cur{0, (int)blockIdx.x / tiles_x, (int)blockIdx.x % tiles_x, 0};
-  blocking_load(cur);
+  blocking_load(cur, 0);
+  int it = 0;
   // the polling warp reads the counters of the items one and two ahead in
   // advance, so the prefetch point rarely waits for an L2 round trip
   unsigned v1 = pw ? poll(adv(cur)) : 0u, v2 = 0u;
@@ -700,8 +691,12 @@ lattice_flow_kernel(int nx, int ny, FlowArgs fa, const uint32_t* __restrict__ bi
       cp_wait<0>();
       __syncthreads();
     }
-    const unsigned m = stage_to_regs<S, V>(stage, tx, ty, vD, vL, vR, vU);
+    // subnormal guard (qwb_lattice.cuh): blocks k % kCheckEvery == 0 test
+    // their inputs, later blocks run exactly once a test in their cone hit
+    const bool check = cur.k % qwb::kCheckEvery == 0;
+    const unsigned m = stage_to_regs<S, V>(stage, tx, ty, vD, vL, vR, vU, check);
     __syncthreads();   // stage consumed
+    const bool all_exact = !check && shw[2 + (it & 1)] != 0;
     const bool more = nxt.k < fa.nblocks;
     // the previous tile's counter: its stores precede the barrier above
     if (pend_tile >= 0) release(pend_tile, pend_val);
@@ -709,9 +704,12 @@ lattice_flow_kernel(int nx, int ny, FlowArgs fa, const uint32_t* __restrict__ bi
     // a wrapping region's cp.async after the first step (shw[0] = 2);
     // otherwise after this tile (shw[0] = 0: it may depend on this tile)
     if (pw && more) {
-      bool ok = __all_sync(0xffffffffu, v1 >= (unsigned)nxt.k);
-      if (!ok) ok = __all_sync(0xffffffffu, poll(nxt) >= (unsigned)nxt.k);   // one fresh poll
-      if (ok) acquire_for_async();
+      bool ok = __all_sync(0xffffffffu, v1 >= need_of(nxt));
+      if (!ok) ok = __all_sync(0xffffffffu, poll(nxt) >= need_of(nxt));   // one fresh poll
+      if (ok) {
+        acquire_for_async();
+        note_sticky((it + 1) & 1);
+      }
       const bool tma = inside(nxt);
       if (ok && tma && pw0) tma_item(nxt);
       if (pw0) shw[0] = ok ? (tma ? 1 : 2) : 0;
@@ -722,8 +720,8 @@ lattice_flow_kernel(int nx, int ny, FlowArgs fa, const uint32_t* __restrict__ bi
       if (more && shw[0] == 2) cp_item(nxt);
     };
     tile_run<SHIFT, MARKED, T, BY, V, false>(nx, ny, n, ny, cur.c * OX, tr * OY, tr * OY, ny - tr * OY, m,
-                                             qwb::kTinyKey, false, in, bits, mk, vD, vL, vR, vU, xD, xU, out, tx, ty,
-                                             tid, after0);
+                                             check ? qwb::kTinyKeyPeriodic : 0u, all_exact, in, bits, mk, vD, vL, vR,
+                                             vU, xD, xU, out, tx, ty, tid, after0, fa.sticky);
     // this tile's counter is published at the next prefetch point (after a
     // barrier that its stores precede), or here when the next item waits
     pend_tile = tr * tiles_x + cur.c;
@@ -734,10 +732,11 @@ lattice_flow_kernel(int nx, int ny, FlowArgs fa, const uint32_t* __restrict__ bi
       __syncthreads();
       release(pend_tile, pend_val);
       pend_tile = -1;
-      blocking_load(nxt);
+      blocking_load(nxt, (it + 1) & 1);
     }
     cur = nxt;
     v1 = v2;
+    ++it;
   }
   __syncthreads();
   if (pend_tile >= 0) release(pend_tile, pend_val);
@@ -871,18 +870,16 @@ int launch_flow_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, double2* a, doub
   const int tiles_x = (nx + OX - 1) / OX, tiles_y = (ny + OY - 1) / OY;
   const int ntiles = tiles_x * tiles_y;
   void* ws;
-  int st = qwb::workspace(ctx, (size_t)ntiles * sizeof(unsigned), s, &ws);
+  int st = qwb::workspace(ctx, (size_t)(ntiles + 1) * sizeof(unsigned), s, &ws);
   if (st) return st;
-  QWB_CUDA(ctx, cudaMemsetAsync(ws, 0, (size_t)ntiles * sizeof(unsigned), s));
+  QWB_CUDA(ctx, cudaMemsetAsync(ws, 0, (size_t)(ntiles + 1) * sizeof(unsigned), s));
   FlowArgs fa;
   fa.buf0 = a;
   fa.buf1 = b;
   fa.done = reinterpret_cast<unsigned*>(ws);
+  fa.sticky = reinterpret_cast<int*>(fa.done + ntiles);
   fa.nblocks = nblocks;
   fa.rot = tiles_y / 2;
-#ifdef QWB_EXP_NOROT
-  fa.rot = 0;
-#endif
   CUtensorMap m0{}, m1{};
   const int use_tma = (cached_map<Sh>(&m0, a, nx, ny) && cached_map<Sh>(&m1, b, nx, ny)) ? 1 : 0;
   const size_t smem = Sh::smem_bytes();

@@ -740,20 +740,12 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
       }
       double2 f[VPT];
       for (; c + 4 <= hs; c += 4) {
-#ifdef QWB_EXP_NOTAKE2
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          take(e);
-          addto(ac[u], e);
-        }
-#else
         take2(e, f);
         addto(ac[0], e);
         addto(ac[1], f);
         take2(e, f);
         addto(ac[2], e);
         addto(ac[3], f);
-#endif
       }
 #pragma unroll
       for (int u = 0; u < 3; ++u)
@@ -767,11 +759,7 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
         const double2* ch = ring + (size_t)s * TILE;
         using Y = std::true_type;
         using N = std::false_type;
-#ifdef QWB_EXP_NOFAST
-        if (false) {
-#else
         if (hs >= 1 && hs + LB - 2 < main_end) {
-#endif
           switch (hs & 3) {
             case 0: fold_own(ch, std::integral_constant<int, 0>{}, Y{}); break;
             case 1: fold_own(ch, std::integral_constant<int, 1>{}, Y{}); break;
@@ -800,20 +788,12 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
         constexpr int R = decltype(Rc)::value;   // slot of partner hs
         int cc = hs;
         for (; cc + 4 <= cme; cc += 4) {
-#ifdef QWB_EXP_NOTAKE2
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            take(e);
-            addto(ac[(R + u) & 3], e);
-          }
-#else
           take2(e, f);
           addto(ac[R & 3], e);
           addto(ac[(R + 1) & 3], f);
           take2(e, f);
           addto(ac[(R + 2) & 3], e);
           addto(ac[(R + 3) & 3], f);
-#endif
         }
 #pragma unroll
         for (int u = 0; u < 3; ++u)
