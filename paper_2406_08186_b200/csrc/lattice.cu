@@ -378,7 +378,7 @@ int qwb_lattice_run(qwb_ctx* ctx, int64_t nx, int64_t ny, int shift, const uint3
     st = QWB_OK;
   } else if (nflow > 0) {
     if (st) return st;
-    k = (int64_t)nflow * depth;
+    k = (int64_t)nflow * 4;   // the flow kernel's depth (lattice_tb.cu kFlowT)
     if (nflow & 1) {
       double2* t = cur;
       cur = nxt;
@@ -506,7 +506,8 @@ int qwb_slab_probability_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int
 int qwb_slab_ghost_rows(int64_t nx, int64_t ny, int64_t ny_local, int64_t n_marked, int* ghost_host) {
   // G = m T ghost rows (m temporally blocked launches per exchange), m <= 4
   // (QWB_SLAB_GHOST_MULT) and G <= the thinnest slab; 0: not available
-  const int d = qwb::lattice_slab_depth(qwb::lattice_tb_depth(nx, ny, n_marked));
+  // slabs run the T = kSlabDepth tile kernel whatever the torus default depth
+  const int d = qwb::lattice_tb_depth(nx, ny, n_marked) > 0 ? qwb::lattice_slab_depth(qwb::kSlabDepth) : 0;
   int g = 0;
   if (d >= 2 && nx >= 64 && ny_local >= d) {
     const char* e = getenv("QWB_SLAB_GHOST_MULT");

@@ -46,6 +46,8 @@
 #include <cudaTypedefs.h>
 #include <string.h>
 
+#include <cmath>
+
 #include "qwb_lattice.cuh"
 
 namespace {
@@ -926,12 +928,16 @@ namespace qwb {
 
 // Steps per temporally blocked launch (0 = single-step kernel only).
 // QWB_LATTICE_T overrides (0, 2..6); QWB_LATTICE_SHAPE the tile shape.
+// Default 6: the tiles are HBM-bound at T = 4 (a tile costs its compulsory
+// bytes' HBM time); at T = 6 each step moves 2/3 of the bytes for 30 % more
+// on-chip adds, and the lower HBM power keeps the SM clock higher under the
+// power cap (2048^2: 25.7 vs 27.9 us/step at 1920 vs 1770 MHz).
 int lattice_tb_depth(int64_t nx, int64_t ny, int64_t n_marked) {
   (void)n_marked;
   static int depth = -1;
   if (depth < 0) {
-    depth = env_int("QWB_LATTICE_T", 4);
-    if (depth < 0 || depth == 1) depth = 4;
+    depth = env_int("QWB_LATTICE_T", 6);
+    if (depth < 0 || depth == 1) depth = 6;
     if (depth > 6) depth = 6;
   }
   if (nx < 64 || ny < 64) return 0;   // tiny lattices: the single-step kernel is launch-bound anyway
@@ -999,19 +1005,27 @@ int lattice_sticky(qwb_ctx* ctx, int** out) {
   return QWB_OK;
 }
 
-// The flow kernel runs untraced torus runs of >= 2 T-step blocks when a
-// block is 2 to 16 waves of tiles (num_sms CTAs): there the per-launch
-// kernel's fixed cost per launch (grid fill, tail, launch gap: ~11 us)
-// dominates; on larger lattices its own per-item scheduling costs more
-// (measured).  QWB_LATTICE_FLOW=0: never, 2: always.
+// The flow kernel (its own depth kFlowT) runs untraced torus runs of >= 2
+// blocks when a block is 2 to 16 waves of tiles (num_sms CTAs) and the
+// per-launch kernel at `depth` would leave more than 10 % of its last wave
+// idle: there the per-launch kernel's fixed cost per launch (grid fill, tail,
+// launch gap: ~11 us) dominates; on larger lattices the flow kernel's own
+// per-item scheduling costs more (measured).
+// QWB_LATTICE_FLOW=0: never, 2: always.
 int lattice_flow_blocks(int64_t nx, int64_t ny, int depth, bool traced, int64_t steps, int num_sms) {
   static const int use = env_int("QWB_LATTICE_FLOW", 1);
-  if (!use || traced || depth != kFlowT || shape_of(false) != 4 || nx < 256 || ny < 256) return 0;
+  if (!use || traced || shape_of(false) != 4 || nx < 256 || ny < 256) return 0;
   using Sh = TbShape<kFlowBY, kFlowV>;
   constexpr int OX = Sh::RX - 2 * kFlowT, OY = Sh::RY - 2 * kFlowT;
   const int64_t ntiles = ((nx + OX - 1) / OX) * ((ny + OY - 1) / OY);
-  if (use == 1 && (ntiles < 2 * (int64_t)num_sms || ntiles >= 16 * (int64_t)num_sms)) return 0;
-  const int64_t nb = steps / depth;
+  if (use == 1) {
+    if (ntiles < 2 * (int64_t)num_sms || ntiles >= 16 * (int64_t)num_sms) return 0;
+    int tx, ty;
+    lattice_tb_tiles(depth, (int)nx, (int)ny, &tx, &ty);
+    const double waves = (double)tx * ty / num_sms;
+    if (waves / std::ceil(waves) >= 0.9) return 0;
+  }
+  const int64_t nb = steps / kFlowT;
   return nb >= 2 ? (int)(nb < (1 << 24) ? nb : (1 << 24)) : 0;
 }
 
