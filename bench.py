@@ -479,20 +479,23 @@ def run_b200(args):
     if single:
         depth = dep.value
         if depth > 0 and knd.value == 2:
-            per_walk = 1 + walk % depth   # one persistent flow launch + remainder single steps
-            kernel = f"lattice_flow_kernel<flipflop, T={depth}, 32x64 region> (persistent, {walk // depth} blocks)"
+            rem = walk % 4   # the flow kernel's blocks are 4 steps; a remainder >= 2 is one tile launch
+            per_walk = 1 + (1 if rem >= 2 else rem)
+            kernel = f"lattice_flow_kernel<flipflop, T=4, 32x64 region> (persistent, {walk // 4} blocks)"
         elif depth > 0:
-            per_walk = walk // depth + walk % depth
+            rem = walk % depth   # a remainder >= 2 is one shallower tile launch
+            per_walk = walk // depth + (1 if rem >= 2 else rem)
             kernel = f"lattice_tb_kernel<flipflop, T={depth}, 32x64 region>"
         else:
             per_walk = walk
             kernel = "lattice_step_kernel<flipflop>"
     elif runner.ghost:
+        from paper_2406_08186_b200 import distributed as DI
         # fused slabs: per exchange of G = mT ghost rows, m launches of T steps
         # (over the owned rows extended by (m-1)T, ..., 0 rows); the last < T
         # steps one at a time
         G = runner.ghost
-        depth = 4
+        depth = DI.slab_depth()
         per_walk = walk // depth + walk % depth   # one T-step launch per T steps, then single steps
         kernel = (f"lattice_tb_kernel<flipflop, T={depth}, 32x64 region> on y-slabs with {G} ghost rows "
                   f"({G // depth} launches per exchange)")
@@ -619,7 +622,7 @@ def run_b200(args):
 
 def measure_c5_sharded(q, dev, local, rank, world, dist):
     """C5 across the ranks (strong scaling): the 8192 x 8192 torus split into
-    y-slabs (fused temporally blocked slabs + NCCL ghost rows), 100 coined
+    y-slabs (fused temporally blocked slabs + NCCL ghost rows), 120 coined
     steps, CUDA-event time on the launch stream, max over ranks."""
     import torch
     from paper_2406_08186_b200 import distributed as DI
@@ -628,19 +631,19 @@ def measure_c5_sharded(q, dev, local, rank, world, dist):
     lat = DI.SlabLattice(eng2, nx, nx, "flipflop", (), rank, world, comm=True)
     lat.a.fill_(1.0 / (2.0 * nx))
     stream = torch.cuda.current_stream(dev)
-    lat.advance(8)
+    lat.advance(24)
     dist.barrier()
     torch.cuda.synchronize(dev)
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record(stream)
-    lat.advance(100)
+    lat.advance(120)
     b.record(stream)
     torch.cuda.synchronize(dev)
     dt = max_over_ranks(a.elapsed_time(b) / 1e3, dist, dev)
     lat.close()
     q.stop_engine(eng2)
-    return {"arc_updates_per_s": 4 * nx * nx * 100 / dt, "us_per_step": dt / 100 * 1e6, "ranks": world,
+    return {"arc_updates_per_s": 4 * nx * nx * 120 / dt, "us_per_step": dt / 120 * 1e6, "ranks": world,
             "ghost_rows": lat.ghost, "rows_per_rank": lat.rows,
             "scaling": "strong (one 8192 x 8192 torus over all ranks)"}
 
@@ -679,11 +682,13 @@ def measure_c4_sharded(q, dev, local, rank, world, dist):
 
 
 def _fused_depth(nx: int, n_marked: int) -> int:
+    """Coined steps per HBM pass of an untraced run (the flow kernel's blocks
+    are 4 steps)."""
     import ctypes as C
     from paper_2406_08186_b200 import _native as N
     dep, knd = C.c_int(0), C.c_int(0)
     N.load().qwb_lattice_fused_depth(nx, nx, n_marked, C.byref(dep), C.byref(knd))
-    return dep.value
+    return 4 if knd.value == 2 else dep.value
 
 
 def measure_extras(q, CO, eng, dev, peak):
@@ -710,9 +715,9 @@ def measure_extras(q, CO, eng, dev, peak):
     spec = q.CoinedSpec(g, "flipflop", "grover", frozenset({c}), "minus_identity")
     r = CO._LatticeRunner(eng, spec)
     r.a.fill_(1.0 / np.sqrt(4 * nx * nx))
-    s = timed(lambda: r.advance(200), 3)
+    s = timed(lambda: r.advance(240), 3)
     arcs = 4 * nx * nx
-    per = s / 600
+    per = s / 720
     T = max(_fused_depth(nx, 1), 1)
     gbs = 32 * arcs / (per * T) / 1e9    # state read + written once per T-step launch
     out["grid4096_marked"] = {"arc_updates_per_s": arcs / per, "achieved_GBps": gbs, "frac": gbs / peak,
@@ -737,10 +742,10 @@ def measure_extras(q, CO, eng, dev, peak):
     del r1
     torch.cuda.empty_cache()
     # C5 on one GPU (the efficiency denominator of the multi-GPU runs):
-    # 8192^2 torus, 8.6 GB ping-pong state, 100 coined steps
+    # 8192^2 torus, 8.6 GB ping-pong state, 120 coined steps
     r5 = CO._LatticeRunner(eng, q.CoinedSpec(q.graphs.grid(8192, 8192)))
     r5.a.fill_(1.0 / (2.0 * 8192))
-    s5 = timed(lambda: r5.advance(100), 2) / 200
+    s5 = timed(lambda: r5.advance(120), 2) / 240
     out["c5_grid8192"] = {"arc_updates_per_s": 4 * 8192 * 8192 / s5, "us_per_step": s5 * 1e6,
                           "state_bytes": 2 * 4 * 8192 * 8192 * 16}
     del r5

@@ -186,8 +186,8 @@ int qwb_slab_probability(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64
 int qwb_slab_step(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int shift,
                   const uint32_t* marked_bits, const qwb_z* in, qwb_z* out, int part, void* stream);
 /* Fused (temporally blocked) slabs: G = qwb_slab_ghost_rows(...) ghost rows
- * each side, G = m T with T = 4 (the slab depth), m = QWB_SLAB_GHOST_MULT (4, <= 8)
- * and G <= the thinnest slab; 0: not available, use the 1-extra-row functions
+ * each side, G = m T with T = qwb_slab_depth() (6), m = QWB_SLAB_GHOST_MULT (4 while
+ * G <= 32) and G <= the thinnest slab; 0: not available, use the 1-extra-row functions
  * above.  Planes hold 4 x nx x (ny_local + 2G) qwb_z, owned rows are local
  * rows [G, G+ny_local).
  * qwb_slab_run_fused: per NCCL exchange of g = jT state rows per plane with
@@ -196,6 +196,8 @@ int qwb_slab_step(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_l
  * side; the last < T steps as single pull steps (1-row exchange).  The same
  * arithmetic as one GPU: bitwise equal.                                       */
 int qwb_slab_ghost_rows(int64_t nx, int64_t ny, int64_t ny_local, int64_t n_marked, int* ghost_host);
+/* T, the coined steps per temporally blocked slab launch                     */
+int qwb_slab_depth(int* depth_host);
 int qwb_slab_to_planes_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,
                          const qwb_z* arcs, qwb_z* planes, void* stream);
 int qwb_slab_from_planes_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t ny_local, int64_t ghost,

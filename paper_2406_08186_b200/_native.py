@@ -80,6 +80,7 @@ SIGNATURES = {
     "qwb_slab_exchange_local": [_vp, _i64, _i32, _p_i64, C.POINTER(_vp), _i32, _vp],
     "qwb_csr_halo_exchange": [_vp, _i64, _vp, _vp, _p_i64, _p_i64, C.POINTER(C.c_int), _i32, _vp, _vp],
     "qwb_slab_ghost_rows": [_i64, _i64, _i64, _i64, _p_int],
+    "qwb_slab_depth": [_p_int],
     "qwb_slab_to_planes_g": [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp],
     "qwb_slab_from_planes_g": [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp],
     "qwb_slab_probability_g": [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp],

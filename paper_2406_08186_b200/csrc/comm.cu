@@ -336,17 +336,34 @@ int qwb_slab_run_fused(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t
     nxt = t;
     ++swaps;
   };
-  auto launch = [&](int nsteps, int ext) -> int {
-    const int st = qwb_slab_advance_local(ctx, nx, ny, y0, ny_local, ghost, shift, marked_bits, marked_host,
-                                          n_marked, reinterpret_cast<qwb_z*>(cur), reinterpret_cast<qwb_z*>(nxt),
-                                          nsteps, ext, stream);
+  // subnormal guard: the first launch after each exchange tests its tiles
+  // (its regions hold every value that reaches an owned row before the next
+  // exchange); a hit switches the rest of the run to numpy's arithmetic
+  int* sticky = nullptr;
+  {
+    const int st = qwb::lattice_sticky(ctx, &sticky);
+    if (st) return st;
+    QWB_CUDA(ctx, cudaMemsetAsync(sticky, 0, sizeof(int), s));
+  }
+  auto geo_of = [&](int ext) {
+    return qwb::TbGeo{(int)(ny_local + 2 * ghost), (int)ghost - ext, (int)ny_local + 2 * ext, (int)(y0 - ext), 0};
+  };
+  auto launch = [&](int nsteps, int ext, int check) -> int {
+    int st;
+    if (nsteps == 1) {
+      st = qwb_slab_advance_local(ctx, nx, ny, y0, ny_local, ghost, shift, marked_bits, marked_host, n_marked,
+                                  reinterpret_cast<qwb_z*>(cur), reinterpret_cast<qwb_z*>(nxt), 1, 0, stream);
+    } else {
+      st = qwb::lattice_tb_launch_geo(ctx, T, shift, s, (int)nx, (int)ny, geo_of(ext), cur, nxt, marked_bits,
+                                      marked_host, n_marked, 0, 0, 0, check, sticky);
+    }
     swap();
     return st;
   };
   // the T-step launch over owned rows + ext, as middle band (during the
   // exchange) and edge bands (after it); false: no middle band here
   auto overlapped = [&](int g, int ext, int* st) -> bool {
-    const qwb::TbGeo geo{(int)(ny_local + 2 * ghost), (int)ghost - ext, (int)ny_local + 2 * ext, (int)(y0 - ext), 0};
+    const qwb::TbGeo geo = geo_of(ext);
     int tx, ty;
     const int oy = qwb::lattice_tb_tiles(T, (int)nx, geo.nown, &tx, &ty);
     // tile row r: local rows own0 + r oy + [-T, oy + T) must lie in the owned rows
@@ -358,7 +375,7 @@ int qwb_slab_run_fused(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t
     auto part = [&](int t0, int t1, int cap) -> int {
       if (t1 <= t0) return QWB_OK;
       return qwb::lattice_tb_launch_geo(ctx, T, shift, s, (int)nx, (int)ny, geo, cur, nxt, marked_bits, marked_host,
-                                        n_marked, t0, t1, cap);
+                                        n_marked, t0, t1, cap, 1, sticky);
     };
     cudaError_t e = cudaEventRecord(ctx->ev_ready, s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ctx->ev_ready, 0);
@@ -382,14 +399,14 @@ int qwb_slab_run_fused(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int64_t
     int st = QWB_OK;
     if (g == 1) {
       st = ghost_exchange_nccl(ctx, nx, ny_local, ghost, 1, cur, rank_below, rank_above, s);
-      if (!st) st = launch(1, 0);
+      if (!st) st = launch(1, 0, 0);
     } else {
       int ext = (int)g - T;
       if (!overlapped((int)g, ext, &st)) {
         st = ghost_exchange_nccl(ctx, nx, ny_local, ghost, (int)g, cur, rank_below, rank_above, s);
-        if (!st) st = launch(T, ext);
+        if (!st) st = launch(T, ext, 1);
       }
-      for (ext -= T; ext >= 0 && !st; ext -= T) st = launch(T, ext);
+      for (ext -= T; ext >= 0 && !st; ext -= T) st = launch(T, ext, 0);
     }
     if (st) return st;
     k += g;

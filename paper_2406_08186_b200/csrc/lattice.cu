@@ -386,22 +386,28 @@ int qwb_lattice_run(qwb_ctx* ctx, int64_t nx, int64_t ny, int shift, const uint3
     }
     swaps += nflow;
   }
-  if (depth > 0 && k + depth <= steps) {
+  if (depth > 0 && steps - k >= 2) {
     // subnormal guard: the first launch and every kCheckEvery-th test the
     // tiles' inputs; a hit switches the rest of the run to numpy's arithmetic
     int* sticky = nullptr;
     st = qwb::lattice_sticky(ctx, &sticky);
     if (st) return st;
     QWB_CUDA(ctx, cudaMemsetAsync(sticky, 0, sizeof(int), s));
-    for (int64_t i = 0; k + depth <= steps; k += depth, ++i) {
-      st = qwb::lattice_tb_launch(ctx, depth, shift, s, (int)nx, (int)ny, cur, nxt, marked_bits,
+    int64_t i = 0;
+    while (steps - k >= 2) {
+      // whole T-step launches, then one shallower launch for a remainder >= 2
+      const int d = steps - k >= depth ? depth : (int)(steps - k);
+      st = qwb::lattice_tb_launch(ctx, d, shift, s, (int)nx, (int)ny, cur, nxt, marked_bits,
                                   marked_host, n_marked, trace_vertices_host, trace ? n_trace : 0,
-                                  trace ? trace + k * n_trace : nullptr, i % qwb::kCheckEvery == 0, sticky);
+                                  trace ? trace + k * n_trace : nullptr, i % qwb::kCheckEvery == 0 || d != depth,
+                                  sticky);
       if (st) return st;
       double2* t = cur;
       cur = nxt;
       nxt = t;
       ++swaps;
+      k += d;
+      ++i;
     }
   }
   for (; k < steps; ++k) {
@@ -503,9 +509,14 @@ int qwb_slab_probability_g(qwb_ctx* ctx, int64_t nx, int64_t ny, int64_t y0, int
   return QWB_OK;
 }
 
+int qwb_slab_depth(int* depth_host) {
+  if (depth_host) *depth_host = qwb::kSlabDepth;
+  return QWB_OK;
+}
+
 int qwb_slab_ghost_rows(int64_t nx, int64_t ny, int64_t ny_local, int64_t n_marked, int* ghost_host) {
-  // G = m T ghost rows (m temporally blocked launches per exchange), m <= 4
-  // (QWB_SLAB_GHOST_MULT) and G <= the thinnest slab; 0: not available
+  // G = m T ghost rows (m temporally blocked launches per exchange), m = 4
+  // (QWB_SLAB_GHOST_MULT, G <= 32) and G <= the thinnest slab; 0: not available
   // slabs run the T = kSlabDepth tile kernel whatever the torus default depth
   const int d = qwb::lattice_tb_depth(nx, ny, n_marked) > 0 ? qwb::lattice_slab_depth(qwb::kSlabDepth) : 0;
   int g = 0;
@@ -515,6 +526,7 @@ int qwb_slab_ghost_rows(int64_t nx, int64_t ny, int64_t ny_local, int64_t n_mark
     if (m < 1) m = 1;
     if (m > 8) m = 8;
     if (m > ny_local / d) m = (int)(ny_local / d);
+    if (m * d > 32) m = 32 / d;   // lattice_slab_geom_g: at most 32 ghost rows
     g = m * d;
   }
   if (ghost_host) *ghost_host = g;

@@ -1052,10 +1052,12 @@ int lattice_tb_owned_rows(int depth) {
 
 int lattice_tb_launch_geo(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny, const TbGeo& geo,
                           const double2* in, double2* out, const uint32_t* bits, const int64_t* marked_host,
-                          int64_t n_marked, int tile0, int tile1, int grid_cap) {
-  // slab launches test every tile's input (their horizon is one launch)
+                          int64_t n_marked, int tile0, int tile1, int grid_cap, int check, int* sticky) {
+  // no run flag: every launch tests its tiles (horizon: one launch);
+  // with one: the run's first launch after each exchange tests (qwb_slab_run_fused)
+  const unsigned key = sticky ? (check ? kTinyKeyPeriodic : 0u) : kTinyKey;
   return tb_launch_impl(ctx, depth, shift, s, nx, ny, geo, in, out, bits, marked_host, n_marked, nullptr, 0,
-                        nullptr, tile0, tile1, kTinyKey, nullptr, grid_cap);
+                        nullptr, tile0, tile1, key, sticky, grid_cap);
 }
 
 int lattice_tb_tiles(int depth, int nx, int nown, int* tiles_x, int* tiles_y) {

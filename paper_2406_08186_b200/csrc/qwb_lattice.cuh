@@ -208,7 +208,7 @@ int lattice_check_shift(qwb_ctx* ctx, int shift);
 // rows [own0, own0 + nown) = global rows [ybase, ybase + nown).  wrap = 1:
 // the buffer is the whole torus (rows wrap inside it); wrap = 0: a slab with
 // >= T ghost rows each side holding the neighbours' state (no wrap).
-constexpr int kSlabDepth = 4;   // the slab (ghost-row) tile kernels are built for this depth
+constexpr int kSlabDepth = 6;   // the slab (ghost-row) tile kernels are built for this depth
 struct TbGeo {
   int lrows, own0, nown, ybase, wrap;
 };
@@ -216,10 +216,13 @@ int lattice_tb_depth(int64_t nx, int64_t ny, int64_t n_marked);
 int lattice_tb_owned_rows(int depth);   // owned rows per tile row of the tile kernel (0: n/a)
 int lattice_slab_depth(int depth);      // ghost-row depth usable by slab runs (0: none)
 // tiles [tile0, tile1) of the launch's tile grid (tile1 = 0: all tiles), on
-// at most grid_cap SMs (0: all)
+// at most grid_cap SMs (0: all).  Subnormal guard: without a run flag every
+// tile tests its input; with one (sticky), `check` launches test against the
+// periodic threshold and the others follow the flag.
 int lattice_tb_launch_geo(qwb_ctx* ctx, int depth, int shift, cudaStream_t s, int nx, int ny, const TbGeo& geo,
                           const double2* in, double2* out, const uint32_t* bits, const int64_t* marked_host,
-                          int64_t n_marked, int tile0, int tile1, int grid_cap = 0);
+                          int64_t n_marked, int tile0, int tile1, int grid_cap = 0, int check = 1,
+                          int* sticky = nullptr);
 // the tile grid of a launch over nown owned rows (row-major tiles); returns
 // the owned rows per tile row
 int lattice_tb_tiles(int depth, int nx, int nown, int* tiles_x, int* tiles_y);

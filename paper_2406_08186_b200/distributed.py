@@ -425,7 +425,7 @@ class SlabLattice:
             self.bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=engine.torch_device)
             mk = torch.tensor(self.marked, dtype=torch.int64, device=engine.torch_device)
             engine.call("qwb_marked_bitmap", n, N.ptr(mk), len(marked), N.ptr(self.bits), engine.stream())
-        # fused path: G ghost state rows each side, G steps per temporally
+        # fused path: G = 4T ghost state rows each side, G steps per temporally
         # blocked launch (the same G on every rank: from the smallest slab)
         self.ghost = slab_ghost_rows(self.nx, self.ny, self.world, len(self.marked))
         size = 4 * self.nx * (self.rows + 2 * (self.ghost or 1))
@@ -484,6 +484,13 @@ class SlabLattice:
             self.engine.call("qwb_comm_destroy")
 
 
+def slab_depth() -> int:
+    """T, the coined steps per temporally blocked slab launch (kSlabDepth)."""
+    t = C.c_int(0)
+    N.check(N.load().qwb_slab_depth(C.byref(t)))
+    return int(t.value)
+
+
 def slab_ghost_rows(nx: int, ny: int, world: int, n_marked: int) -> int:
     """Ghost rows G of the fused (temporally blocked) slab path, 0 when it is
     not available (tiny lattices, slabs thinner than G rows, or
@@ -527,7 +534,7 @@ def emulate_slabs_fused(engine: Engine, nx: int, ny: int, world: int, psi_arcs: 
         cur.append(a)
         nxt.append(b)
     nl = N.i64_array([r for (_, r) in parts])
-    T = 4   # the slab depth (kSlabDepth); G = m T
+    T = slab_depth()   # G = m T
 
     def launch(nsteps, ext):
         nonlocal cur, nxt
