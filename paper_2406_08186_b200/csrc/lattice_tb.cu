@@ -87,6 +87,16 @@ __device__ __forceinline__ void acquire_for_async() {
   asm volatile("fence.proxy.async.global;\n" ::: "memory");
 }
 
+#ifdef QWB_EXP_TIMING
+__device__ unsigned long long g_dbg[2][8];   // [kernel: 0 tile, 1 flow][slot]
+__device__ __forceinline__ unsigned long long dbg_clock() { return clock64(); }
+#define DBG_T(var) const unsigned long long var = dbg_clock()
+#define DBG_ADD(k, slot, v) atomicAdd(&g_dbg[k][slot], (unsigned long long)(v))
+#else
+#define DBG_T(var)
+#define DBG_ADD(k, slot, v)
+#endif
+
 __device__ __forceinline__ int wrapc(int v, int n) {
   v = v < 0 ? v + n : v;
   return v >= n ? v - n : v;
@@ -353,19 +363,70 @@ __device__ __forceinline__ unsigned stage_to_regs(const double2* stage, int tx, 
   return m;
 }
 
+// The tile's T steps in numpy's own arithmetic (halve, then sum: the
+// reference's bits in the subnormal range too), its region loaded from `in`
+// (intact while the tile runs: a launch writes the other buffer, and a flow
+// item's input region is not overwritten before the item is done), owned
+// block stored.  Out of line: the rare path stays out of the hot kernel body
+// (instruction-cache footprint).
+template <int SHIFT, bool MARKED, int T, int BY, int V, bool SLAB>
+__device__ __noinline__ void tile_exact(int nx, int ny, int64_t n, int lrows, int x0, int y0, int lyb, int rows_left,
+                                        bool interior, const double2* __restrict__ in,
+                                        const uint32_t* __restrict__ bits, double2* xD, double2* xU,
+                                        double2* __restrict__ out) {
+  using S = TbShape<BY, V>;
+  constexpr int OX = S::RX - 2 * T, OY = S::RY - 2 * T;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  const int gx = wrapc(x0 - T + tx, nx);
+  int gy[V];
+  double2 vD[V], vL[V], vR[V], vU[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    gy[j] = wrapc(y0 - T + ty * V + j, ny);
+    const int ly = lyb - T + ty * V + j;   // local buffer row
+    const bool ok = !SLAB || (ly >= 0 && ly < lrows);
+    const int64_t w = (int64_t)(SLAB ? (ok ? ly : 0) : wrapc(ly, ny)) * nx + gx;
+    const double2 z = make_double2(0.0, 0.0);
+    // L2 loads (.cg): in the persistent kernel an L1 line of this buffer can
+    // be two blocks old; the region's current values were published to L2
+    // before the item's dependencies were acquired
+    vD[j] = ok ? __ldcg(in + w) : z;
+    vL[j] = ok ? __ldcg(in + n + w) : z;
+    vR[j] = ok ? __ldcg(in + 2 * n + w) : z;
+    vU[j] = ok ? __ldcg(in + 3 * n + w) : z;
+  }
+  if (interior)
+    tile_steps<SHIFT, false, T, BY, V, true, true>(nx, ny, gx, gy, 0u, 0u, bits, vD, vL, vR, vU, xD, xU, tid, ty,
+                                                   NoHook{});
+  else
+    tile_steps<SHIFT, MARKED, T, BY, V, false, true>(nx, ny, gx, gy, 0u, 0u, bits, vD, vL, vR, vU, xD, xU, tid, ty,
+                                                     NoHook{});
+  const bool col_ok = tx >= T && tx < T + OX && x0 + tx - T < nx;
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    const int ly = ty * V + j;
+    if (col_ok && ly >= T && ly < T + OY && ly - T < rows_left) {
+      const int64_t w = (int64_t)(lyb - T + ly) * nx + gx;
+      __stcs(out + w, vD[j]);
+      __stcs(out + n + w, vL[j]);
+      __stcs(out + 2 * n + w, vR[j]);
+      __stcs(out + 3 * n + w, vU[j]);
+    }
+  }
+}
+
 // Steps + store of one tile whose registers are loaded.  (x0, y0): global
 // column / unwrapped global row of its first owned vertex; lyb: local buffer
 // row of that row; rows_left: owned rows from y0 to the end of the launch's
-// owned range; m: the threads' tiny-input flags (stage_to_regs).  The steps
-// run in doubled space; if any input amplitude of the region is tiny (rare:
-// the front of a localized start after ~1000 steps) the region is reloaded
-// from `in` (intact during the tile: the launch writes the other buffer, and
-// a flow item's input region is not overwritten before the item is done) and
-// the steps are redone in numpy's arithmetic.  The check is off the critical
-// path: its integer work interleaves with the first step, its reduction rides
-// on that step's barrier.
+// owned range; m: the threads' tiny-input flags (stage_to_regs), tested
+// against `key` (0: no test).  The steps run in doubled space; if any input
+// amplitude of the region is tiny (rare: the front of a localized start after
+// ~1000 steps) the tile is redone in numpy's arithmetic (tile_exact), as it is
+// from the start when all_exact.  The test is off the critical path: its
+// integer work interleaves with the first step, its reduction rides on that
+// step's barrier.  Returns whether numpy's arithmetic was used.
 template <int SHIFT, bool MARKED, int T, int BY, int V, bool SLAB, class F>
-__device__ __forceinline__ void tile_run(int nx, int ny, int64_t n, int lrows, int x0, int y0, int lyb,
+__device__ __forceinline__ bool tile_run(int nx, int ny, int64_t n, int lrows, int x0, int y0, int lyb,
                                          int rows_left, unsigned m, unsigned key, bool all_exact,
                                          const double2* __restrict__ in,
                                          const uint32_t* __restrict__ bits, const MarkedList& mk,
@@ -391,41 +452,25 @@ __device__ __forceinline__ void tile_run(int nx, int ny, int64_t n, int lrows, i
       }
     }
   }
-  bool tiny = all_exact;
   if (all_exact) {   // a run that met tiny amplitudes: numpy's arithmetic from the start
-    if (interior)
-      tile_steps<SHIFT, false, T, BY, V, true, true>(nx, ny, gx, gy, 0u, 0u, bits, vD, vL, vR, vU, xD, xU, tid, ty,
-                                                     after0);
-    else
-      tile_steps<SHIFT, MARKED, T, BY, V, false, true>(nx, ny, gx, gy, 0u, 0u, bits, vD, vL, vR, vU, xD, xU, tid,
-                                                       ty, after0);
-  } else {
-    tiny = interior ? tile_steps<SHIFT, false, T, BY, V, true, false>(nx, ny, gx, gy, m, key, bits, vD, vL, vR, vU, xD,
-                                                                      xU, tid, ty, after0)
-                    : tile_steps<SHIFT, MARKED, T, BY, V, false, false>(nx, ny, gx, gy, m, key, bits, vD, vL, vR, vU,
-                                                                        xD, xU, tid, ty, after0);
+    __syncthreads();   // after0 reads what the flow kernel's polling warp decided just before
+    after0();
+    tile_exact<SHIFT, MARKED, T, BY, V, SLAB>(nx, ny, n, lrows, x0, y0, lyb, rows_left, interior, in, bits, xD, xU,
+                                              out);
+    return true;
   }
-  if (tiny && !all_exact) {
+  const bool tiny =
+      interior ? tile_steps<SHIFT, false, T, BY, V, true, false>(nx, ny, gx, gy, m, key, bits, vD, vL, vR, vU, xD,
+                                                                 xU, tid, ty, after0)
+               : tile_steps<SHIFT, MARKED, T, BY, V, false, false>(nx, ny, gx, gy, m, key, bits, vD, vL, vR, vU, xD,
+                                                                   xU, tid, ty, after0);
+  if (tiny) {
     if (sticky && tid == 0) atomicOr(sticky, 1);
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      const int ly = lyb - T + ty * V + j;   // local buffer row
-      const bool ok = !SLAB || (ly >= 0 && ly < lrows);
-      const int64_t w = (int64_t)(SLAB ? (ok ? ly : 0) : wrapc(ly, ny)) * nx + gx;
-      const double2 z = make_double2(0.0, 0.0);
-      vD[j] = ok ? in[w] : z;
-      vL[j] = ok ? in[n + w] : z;
-      vR[j] = ok ? in[2 * n + w] : z;
-      vU[j] = ok ? in[3 * n + w] : z;
-    }
-    if (interior)
-      tile_steps<SHIFT, false, T, BY, V, true, true>(nx, ny, gx, gy, 0u, 0u, bits, vD, vL, vR, vU, xD, xU, tid, ty,
-                                                     NoHook{});
-    else
-      tile_steps<SHIFT, MARKED, T, BY, V, false, true>(nx, ny, gx, gy, 0u, 0u, bits, vD, vL, vR, vU, xD, xU, tid, ty,
-                                                       NoHook{});
+    tile_exact<SHIFT, MARKED, T, BY, V, SLAB>(nx, ny, n, lrows, x0, y0, lyb, rows_left, interior, in, bits, xD, xU,
+                                              out);
+    return true;
   }
-  const double sc = tiny ? 1.0 : 1.0 / (double)(1 << T);   // undo the doubled-space steps (exact)
+  constexpr double sc = 1.0 / (double)(1 << T);   // undo the doubled-space steps (exact)
   const bool col_ok = tx >= T && tx < T + OX && x0 + tx - T < nx;
 #pragma unroll
   for (int j = 0; j < V; ++j) {
@@ -438,6 +483,7 @@ __device__ __forceinline__ void tile_run(int nx, int ny, int64_t n, int lrows, i
       __stcs(out + 3 * n + w, make_double2(__dmul_rn(vU[j].x, sc), __dmul_rn(vU[j].y, sc)));
     }
   }
+  return false;
 }
 
 // ---------------------------------------------------------------------------
@@ -524,6 +570,7 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
     const int x0 = tcol * OX, y0 = geo.ybase + trow_now * OY, lyb = geo.own0 + trow_now * OY;
     advance(tcol, trow);
     double2 vD[V], vL[V], vR[V], vU[V];
+    DBG_T(t_a);
     if (inside(tcol_now, trow_now)) {
       tb_mbar_wait(tbar + k, (ph >> k) & 1u);
       ph ^= 1u << k;
@@ -531,8 +578,10 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
       cp_wait<S::NSTAGE - 1>();   // this stage's group; the other stage's may fly
       __syncthreads();
     }
+    DBG_T(t_b);
     const unsigned m = stage_to_regs<S, V>(stage0 + (size_t)k * 4 * S::REG, tx, ty, vD, vL, vR, vU, check);
     __syncthreads();   // stage k consumed
+    DBG_T(t_c);
     if (ptile < ntiles)
       issue(k, pcol, prow);
     else
@@ -542,6 +591,16 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
     tile_run<SHIFT, MARKED, T, BY, V, SLAB>(nx, ny, n, geo.lrows, x0, y0, lyb, geo.nown - trow_now * OY, m, key,
                                             all_exact, in, bits, mk, vD, vL, vR, vU, xD, xU, out, tx, ty, tid,
                                             NoHook{}, sticky);
+#ifdef QWB_EXP_TIMING
+    DBG_T(t_d);
+    if (tid == 0) {
+      DBG_ADD(0, 0, t_b - t_a);
+      DBG_ADD(0, 1, t_c - t_b);
+      DBG_ADD(0, 2, t_d - t_c);
+      DBG_ADD(0, 3, 1);
+    }
+    if (tid == 32 * 7) DBG_ADD(0, 4, dbg_clock() - t_c);   // a storing warp
+#endif
   }
 }
 
@@ -559,8 +618,9 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
 struct FlowArgs {
   double2* buf0;      // block k reads buf[k & 1], writes buf[(k + 1) & 1]
   double2* buf1;
-  unsigned* done;     // [ntiles] blocks completed per tile (zeroed before the launch)
-  int* sticky;        // subnormal guard: a check block met tiny amplitudes (zeroed before the launch)
+  // [ntiles] per tile: blocks completed (bits 0..30) and, bit 31, the
+  // subnormal flag of its last block (zeroed before the launch)
+  unsigned* done;
   int nblocks;
   int rot;            // tile-row rotation per block
 };
@@ -585,7 +645,7 @@ lattice_flow_kernel(int nx, int ny, FlowArgs fa, const uint32_t* __restrict__ bi
   double2* xU = xD + 2 * S::NT;
   uint64_t* tbar = reinterpret_cast<uint64_t*>(xU + 2 * S::NT);
   // [0]: the next item's load state (0 / 1 TMA / 2 cp.async); [2 + (it & 1)]:
-  // the run's sticky subnormal flag as seen by iteration it's item
+  // iteration it's item inherits the subnormal flag (from its dependencies)
   int* shw = reinterpret_cast<int*>(tbar + 2);
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * 32 + tx;
@@ -621,7 +681,10 @@ lattice_flow_kernel(int nx, int ny, FlowArgs fa, const uint32_t* __restrict__ bi
     const unsigned* q = dep_ptr(p);
     return q ? ld_relaxed(q) : 0xffffffffu;
   };
+
   auto need_of = [&](const FlowPos& p) -> unsigned { return (unsigned)p.k; };
+  constexpr unsigned kFlag = 0x80000000u;   // counter bit 31: the tile's block ran numpy's arithmetic
+  auto done_ok = [&](unsigned v, unsigned need) { return (v & ~kFlag) >= need; };
   auto inside = [&](const FlowPos& p) {
     return region_inside<S>(nx, ny, p.c * OX - T, trow(p) * OY - T, use_tma != 0);
   };
@@ -639,17 +702,22 @@ lattice_flow_kernel(int nx, int ny, FlowArgs fa, const uint32_t* __restrict__ bi
   const bool pw = ty == BY - 1;       // polling warp
   const bool pw0 = pw && tx == 0;
   // all threads: wait until the item's dependencies are done, then load it
-  // after acquiring an item's dependencies: the sticky flag its block sees
-  // (any earlier check item of its dependency cone that met tiny amplitudes
-  // raised it before publishing its counter)
-  auto note_sticky = [&](int slot) {
-    if (pw0) shw[2 + slot] = *reinterpret_cast<volatile int*>(fa.sticky);
+  // Subnormal guard: blocks k % kCheckEvery == 0 test their inputs; a tile
+  // that ran numpy's arithmetic publishes bit 31 with its counter, and an item
+  // of a later block inherits it from its dependencies (cone by cone), until
+  // the next check block (qwb_lattice.cuh).  The polling warp records, with
+  // the counters it observed, whether the item inherits the flag.
+  auto note_flag = [&](const FlowPos& p, unsigned v, int slot) {
+    // lanes without a dependency read 0xffffffff: not a flag
+    const unsigned any = __ballot_sync(0xffffffffu, dep_ptr(p) != nullptr && (v & kFlag) != 0u);
+    if (pw0) shw[2 + slot] = any != 0u;
   };
   auto blocking_load = [&](const FlowPos& p, int slot) {
     if (pw) {
-      while (!__all_sync(0xffffffffu, poll(p) >= need_of(p))) __nanosleep(64);
+      unsigned v;
+      while (!__all_sync(0xffffffffu, done_ok(v = poll(p), need_of(p)))) __nanosleep(64);
       acquire_for_async();
-      note_sticky(slot);
+      note_flag(p, v, slot);
     }
     __syncthreads();   // the other threads' loads are ordered after the polling warp's acquire
     if (inside(p)) {
@@ -678,6 +746,8 @@ lattice_flow_kernel(int nx, int ny, FlowArgs fa, const uint32_t* __restrict__ bi
   int it = 0;
   // the polling warp reads the counters of the items one and two ahead in
   // advance, so the prefetch point rarely waits for an L2 round trip
+  // the polling warp reads the counters of the next item in advance (at the
+  // end of the previous item)
   unsigned v1 = pw ? poll(adv(cur)) : 0u, v2 = 0u;
   uint32_t ph = 0;
   int pend_tile = -1;   // finished tile whose counter is not yet published
@@ -686,6 +756,7 @@ lattice_flow_kernel(int nx, int ny, FlowArgs fa, const uint32_t* __restrict__ bi
     const FlowPos nxt = adv(cur);
     const int tr = trow(cur);
     double2 vD[V], vL[V], vR[V], vU[V];
+    DBG_T(t_a);
     if (inside(cur)) {
       tb_mbar_wait(tbar, ph);
       ph ^= 1u;
@@ -693,11 +764,13 @@ lattice_flow_kernel(int nx, int ny, FlowArgs fa, const uint32_t* __restrict__ bi
       cp_wait<0>();
       __syncthreads();
     }
+    DBG_T(t_b);
     // subnormal guard (qwb_lattice.cuh): blocks k % kCheckEvery == 0 test
     // their inputs, later blocks run exactly once a test in their cone hit
     const bool check = cur.k % qwb::kCheckEvery == 0;
     const unsigned m = stage_to_regs<S, V>(stage, tx, ty, vD, vL, vR, vU, check);
     __syncthreads();   // stage consumed
+    DBG_T(t_c);
     const bool all_exact = !check && shw[2 + (it & 1)] != 0;
     const bool more = nxt.k < fa.nblocks;
     // the previous tile's counter: its stores precede the barrier above
@@ -706,28 +779,46 @@ lattice_flow_kernel(int nx, int ny, FlowArgs fa, const uint32_t* __restrict__ bi
     // a wrapping region's cp.async after the first step (shw[0] = 2);
     // otherwise after this tile (shw[0] = 0: it may depend on this tile)
     if (pw && more) {
-      bool ok = __all_sync(0xffffffffu, v1 >= need_of(nxt));
-      if (!ok) ok = __all_sync(0xffffffffu, poll(nxt) >= need_of(nxt));   // one fresh poll
+      unsigned v = v1;
+      bool ok = __all_sync(0xffffffffu, done_ok(v, need_of(nxt)));
+      if (!ok) ok = __all_sync(0xffffffffu, done_ok(v = poll(nxt), need_of(nxt)));   // one fresh poll
       if (ok) {
         acquire_for_async();
-        note_sticky((it + 1) & 1);
+        note_flag(nxt, v, (it + 1) & 1);
       }
       const bool tma = inside(nxt);
       if (ok && tma && pw0) tma_item(nxt);
       if (pw0) shw[0] = ok ? (tma ? 1 : 2) : 0;
+#ifdef QWB_EXP_TIMING
+      if (pw0) {
+        DBG_ADD(1, 5, ok ? 0 : 1);
+        DBG_ADD(1, 6, dbg_clock() - t_c);
+      }
+#endif
     }
     const double2* in = (cur.k & 1) ? fa.buf1 : fa.buf0;
     double2* out = (cur.k & 1) ? fa.buf0 : fa.buf1;
     auto after0 = [&]() {
       if (more && shw[0] == 2) cp_item(nxt);
     };
-    tile_run<SHIFT, MARKED, T, BY, V, false>(nx, ny, n, ny, cur.c * OX, tr * OY, tr * OY, ny - tr * OY, m,
-                                             check ? qwb::kTinyKeyPeriodic : 0u, all_exact, in, bits, mk, vD, vL, vR,
-                                             vU, xD, xU, out, tx, ty, tid, after0, fa.sticky);
+    const bool exact_used =
+        tile_run<SHIFT, MARKED, T, BY, V, false>(nx, ny, n, ny, cur.c * OX, tr * OY, tr * OY, ny - tr * OY, m,
+                                                 check ? qwb::kTinyKeyPeriodic : 0u, all_exact, in, bits, mk, vD, vL,
+                                                 vR, vU, xD, xU, out, tx, ty, tid, after0);
+#ifdef QWB_EXP_TIMING
+    DBG_T(t_d);
+    if (tid == 0) {
+      DBG_ADD(1, 0, t_b - t_a);
+      DBG_ADD(1, 1, t_c - t_b);
+      DBG_ADD(1, 2, t_d - t_c);
+      DBG_ADD(1, 3, 1);
+    }
+    if (tid == 32 * 7) DBG_ADD(1, 4, dbg_clock() - t_c);
+#endif
     // this tile's counter is published at the next prefetch point (after a
     // barrier that its stores precede), or here when the next item waits
     pend_tile = tr * tiles_x + cur.c;
-    pend_val = (unsigned)cur.k + 1;
+    pend_val = ((unsigned)cur.k + 1) | (exact_used ? kFlag : 0u);
     if (!more) break;
     if (pw) v2 = poll(adv(nxt));
     if (shw[0] == 0) {
@@ -879,7 +970,6 @@ int launch_flow_t(qwb_ctx* ctx, cudaStream_t s, int nx, int ny, double2* a, doub
   fa.buf0 = a;
   fa.buf1 = b;
   fa.done = reinterpret_cast<unsigned*>(ws);
-  fa.sticky = reinterpret_cast<int*>(fa.done + ntiles);
   fa.nblocks = nblocks;
   fa.rot = tiles_y / 2;
   CUtensorMap m0{}, m1{};
@@ -1083,3 +1173,14 @@ extern "C" int qwb_lattice_fused_depth(int64_t nx, int64_t ny, int64_t n_marked,
   if (kind_host) *kind_host = (d > 0 && qwb::lattice_flow_blocks(nx, ny, d, false, 2 * d, sms)) ? 2 : 1;
   return QWB_OK;
 }
+
+#ifdef QWB_EXP_TIMING
+extern "C" int qwb_exp_dbg(unsigned long long* out_host, int reset) {
+  cudaMemcpyFromSymbol(out_host, g_dbg, sizeof(g_dbg));
+  if (reset) {
+    unsigned long long z[2][8] = {};
+    cudaMemcpyToSymbol(g_dbg, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
