@@ -472,11 +472,14 @@ __device__ __noinline__ double2 hc_marked_row(const HcStreamArgs& a, double g, c
   return sr.result();
 }
 
-// NS: ring stages; SPLIT: producer lanes, each copying 1/SPLIT of a chunk;
-// CONS: consumer threads (+ one producer warp + one fix-up warp), TILE / CONS
-// vertices each
-template <int NS, int SPLIT, int CONS>
-__global__ void __launch_bounds__(CONS + 64, 1)
+// NS: ring stages; PROD: producer warps (one issuing lane each; producer q
+// issues the ring chunks it == q mod PROD, producer 0 also the acc tiles);
+// CONS: consumer threads (+ PROD producer warps + one fix-up warp), TILE / CONS
+// vertices each.  A single issuing thread tops out near one 16-KB chunk per
+// ~330 cycles (its wait -> expect_tx -> copy chain), below the SM's share of
+// the L2 bandwidth; two interleaved producers overlap their chains.
+template <int NS, int PROD, int CONS>
+__global__ void __launch_bounds__(CONS + 32 * PROD + 32, 1)
 hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* __restrict__ tin, double2* __restrict__ tout,
                  const double2* acc_in, double2* acc_out, double s_k, const int* __restrict__ done,
                  double* __restrict__ partial) {
@@ -492,7 +495,7 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
   // [2][32]: per acc slot, the tile's marked-bitmap words (bulk-copied with
   // the acc tile)
   uint32_t* awords = reinterpret_cast<uint32_t*>(aempty + 2);
-  __shared__ double red[CONS / 32 + 2];
+  __shared__ double red[CONS / 32 + PROD + 1];
   const int tid = threadIdx.x;
   const int dim = op.dim;
   const int nh = dim - LB;                            // high bits (global)
@@ -524,30 +527,23 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
 
   if (tid >= CONS) {
     const int pl = tid - CONS;
-    if (pl < SPLIT) {   // (lanes SPLIT..31 of the producer warp idle)
-      // ---------------- producer lanes: stream the partner tiles in row order
-      constexpr unsigned pmask = (SPLIT == 32) ? 0xffffffffu : ((1u << SPLIT) - 1u);
-      constexpr uint32_t part = CHUNK_BYTES / SPLIT;
-      auto issue = [&](uint64_t* fb, double2* dst, const double2* src, uint32_t extra) {
-        if (pl == 0) mbar_expect_tx(fb, CHUNK_BYTES + extra);
-        __syncwarp(pmask);
-        bulk_g2s(reinterpret_cast<char*>(dst) + pl * part, reinterpret_cast<const char*>(src) + pl * part,
-                 part, fb);
-      };
-      uint32_t it = 0, ti = 0;
+    if (pl < 32 * PROD && (pl & 31) == 0) {   // (lanes 1..31 of the producer warps idle)
+      // ---------------- producers: stream the partner tiles in row order
+      const uint32_t q = (uint32_t)pl >> 5;
+      uint32_t s = 0, ph = 0, ti = 0, it = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
         const uint32_t Hl = (uint32_t)tile, H = hbase | Hl;
         const int hs = __popc(H);
-        {   // the tile's acc values and (marked runs) its 32 bitmap words,
-            // consumed in the epilogue; both complete on the acc slot's barrier
+        if (q == 0) {   // the tile's acc values and (marked runs) its 32 bitmap words,
+                        // consumed in the epilogue; both complete on the acc slot's barrier
           const int ab = ti & 1;
           mbar_wait(aempty + ab, ((ti >> 1) & 1) ^ 1);
-          issue(afull + ab, accbuf + (size_t)ab * TILE, acc_in + ((int64_t)Hl << LB), op.bits ? 128u : 0u);
-          if (op.bits && pl == 0)
-            bulk_g2s(awords + ab * 32, op.bits + ((vbase + (tile << LB)) >> 5), 128u, afull + ab);
+          mbar_expect_tx(afull + ab, CHUNK_BYTES + (op.bits ? 128u : 0u));
+          bulk_g2s(accbuf + (size_t)ab * TILE, acc_in + ((int64_t)Hl << LB), CHUNK_BYTES, afull + ab);
+          if (op.bits) bulk_g2s(awords + ab * 32, op.bits + ((vbase + (tile << LB)) >> 5), 128u, afull + ab);
         }
         uint32_t setm = H, clrm = (~H) & hmask;
-        for (int c = 0; c <= nh; ++c) {
+        for (int c = 0; c <= nh; ++c, ++it) {
           int b = -1;   // partner across high bit b (-1: the tile itself)
           if (c < hs) {
             b = 31 - __clz(setm);
@@ -556,22 +552,27 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
             b = __ffs(clrm) - 1;
             clrm ^= 1u << b;
           }
+          const uint32_t sc = s, pc = ph;
+          if (++s == NS) {
+            s = 0;
+            ph ^= 1u;
+          }
+          if (PROD > 1 && it % PROD != q) continue;
           const double2* src = b < 0 ? tin + ((int64_t)Hl << LB)
                                : b < nh_loc ? tin + ((int64_t)(Hl ^ (1u << b)) << LB)
                                             : op.remote[b - nh_loc] + ((int64_t)Hl << LB);
-          const int s = it % NS;
-          mbar_wait(empty + s, ((it / NS) & 1) ^ 1);
-          issue(full + s, ring + (size_t)s * TILE, src, 0u);
-          ++it;
+          mbar_wait(empty + sc, pc ^ 1);
+          mbar_expect_tx(full + sc, CHUNK_BYTES);
+          bulk_g2s(ring + (size_t)sc * TILE, src, CHUNK_BYTES, full + sc);
         }
       }
-    } else if (pl >= 32 && op.bits) {
+    } else if (pl >= 32 * PROD && op.bits) {
       // ---------------- fix-up warp: marked rows of this CTA's tiles (the
       // consumers leave those vertices alone).  Its own warp: sharing the
       // producer's warp, the bitmap scan held up the stream (+15 us/term).
       // The lanes scan the bitmap words together; per marked vertex the warp
       // computes the row cooperatively and lane 0 stores it.
-      const int fl = pl - 32;
+      const int fl = pl - 32 * PROD;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint32_t word = __ldg(op.bits + ((vbase + (tile << LB)) >> 5) + fl);   // TILE / 32 == 32 words
         unsigned any = __ballot_sync(0xffffffffu, word != 0u);
@@ -837,40 +838,37 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
   __syncthreads();
   if (tid == 0) {
     double r = 0.0;
-    for (int w = 0; w < CONS / 32 + 2; ++w) r = __dadd_rn(r, red[w]);
+    for (int w = 0; w < CONS / 32 + PROD + 1; ++w) r = __dadd_rn(r, red[w]);
     partial[blockIdx.x] = r;
   }
 }
 
 // launch one term; returns the number of partials the kernel wrote
-template <int NS, int SPLIT, int CONS>
+template <int NS, int PROD, int CONS>
 void launch_stream(const HcStream& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
                    const double2* ain, double2* acc, double s_k, const int* flags, double* partial) {
   static bool configured[256] = {};
   const int dev = op.device & 255;
   if (!configured[dev]) {
-    cudaFuncSetAttribute(hc_stream_kernel<NS, SPLIT, CONS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(hc_stream_kernel<NS, PROD, CONS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)hcs::smem_bytes(NS));
     configured[dev] = true;
   }
-  launch_pdl(hc_stream_kernel<NS, SPLIT, CONS>, op.grid, CONS + 64, hcs::smem_bytes(NS), s, op, n, tin, tout,
+  launch_pdl(hc_stream_kernel<NS, PROD, CONS>, op.grid, CONS + 32 * PROD + 32, hcs::smem_bytes(NS), s, op, n, tin, tout,
              ain, acc, s_k, flags, partial);
 }
 
 int launch_term(const HcStream& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
                 const double2* ain, double2* acc, double s_k, const int* flags, double* partial) {
-  // QWB_HC_STREAM = CONS/256 * 10000 + NS * 100 + SPLIT (tuning knob; measured at
-  // dim 22: 601 173, 20601 157, 20801 143-144.5, 21001 139.6, 21201 140.7,
-  // 20804 166 us/term; with the separate fix-up warp: 11001 141.7, 20801
-  // 117.6, 21001 111.4-111.7, 21201 109.8-110.5)
+  // QWB_HC_STREAM = CONS/256 * 10000 + NS * 100 + PROD (tuning knob; dim 22,
+  // us/term on one box: 21201 105.4, 21202 92.5, 21203 102.5 (96 registers,
+  // spills), 21002 94.5; profiles/r02_hc_producers.txt)
   switch (op.variant) {
-    case 601: launch_stream<6, 1, 256>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
-    case 20601: launch_stream<6, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
-    case 11001: launch_stream<10, 1, 256>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
     case 21001: launch_stream<10, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
-    case 20804: launch_stream<8, 4, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
-    case 20801: launch_stream<8, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
-    default: launch_stream<12, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+    case 21002: launch_stream<10, 2, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+    case 21201: launch_stream<12, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+    case 21203: launch_stream<12, 3, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+    default: launch_stream<12, 2, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
   }
   return op.grid;
 }
@@ -1106,7 +1104,7 @@ int hc_stream_base(qwb_ctx* ctx, int dim, int S, double gamma, const uint32_t* b
   static int variant = -1;
   if (variant < 0) {
     const char* e = getenv("QWB_HC_STREAM");
-    variant = (e && *e) ? atoi(e) : 21201;
+    variant = (e && *e) ? atoi(e) : 21202;
   }
   const int64_t ntiles = 1LL << (dim - S - hcs::LB);
   *op = HcStream{};
