@@ -365,6 +365,11 @@ constexpr uint32_t CHUNK_BYTES = TILE * sizeof(double2);
 constexpr size_t smem_bytes(int ns) {
   return (size_t)(ns + 2) * CHUNK_BYTES + (2 * ns + 4) * sizeof(uint64_t) + 2 * 32 * sizeof(uint32_t);
 }
+// paired form: NSP ring stages of two partner chunks + per tile slot (two
+// slots) the acc tile and the own tile, barriers, bitmap words
+constexpr size_t pair_smem_bytes(int nsp) {
+  return (size_t)(2 * nsp + 4) * CHUNK_BYTES + (2 * nsp + 4) * sizeof(uint64_t) + 2 * 32 * sizeof(uint32_t);
+}
 }  // namespace hcs
 
 __device__ __forceinline__ uint32_t nctaid_x() {
@@ -843,6 +848,353 @@ hc_stream_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* 
   }
 }
 
+// Paired form of the streamed hypercube term (nh = dim - LB even, e.g. the
+// C4 dimension 22).  The own tile travels with the acc tile in a per-tile
+// slot, so the ring carries exactly the nh partner tiles, TWO per stage behind
+// one barrier pair: a consumer warp waits, reads and releases once per two
+// partner tiles.  Partner k (row order: set bits high->low, then clear bits
+// low->high) sits at row position k (k < hs) or k + LB (k >= hs), so its
+// numpy accumulator slot is (k + 3) & 3 before the own tile and (k + LB - 1)
+// & 3 after it: with partners taken four at a time from k = 0 every slot is
+// a compile-time register, and only the group holding the own tile (k = hs)
+// branches on hs & 3.
+template <int NSP, int PROD, int CONS>
+__global__ void __launch_bounds__(CONS + 32 * PROD + 32, 1)
+hc_pair_kernel(const __grid_constant__ HcStream op, int64_t n, const double2* __restrict__ tin, double2* __restrict__ tout,
+               const double2* acc_in, double2* acc_out, double s_k, const int* __restrict__ done,
+               double* __restrict__ partial) {
+  using namespace hcs;
+  constexpr int VPT = TILE / CONS;
+  static_assert(LB % 4 == 2, "slot rule below assumes (k + LB - 1) & 3 == (k + 1) & 3");
+  extern __shared__ __align__(128) unsigned char hcs_smem[];
+  double2* ring = reinterpret_cast<double2*>(hcs_smem);                // [NSP][2][TILE]
+  double2* slotbuf = ring + (size_t)2 * NSP * TILE;                    // [2][acc, own][TILE]
+  uint64_t* full = reinterpret_cast<uint64_t*>(hcs_smem + (size_t)(2 * NSP + 4) * CHUNK_BYTES);
+  uint64_t* empty = full + NSP;
+  uint64_t* afull = empty + NSP;                                       // [2]
+  uint64_t* aempty = afull + 2;                                        // [2]
+  uint32_t* awords = reinterpret_cast<uint32_t*>(aempty + 2);          // [2][32]
+  __shared__ double red[CONS / 32 + PROD + 1];
+  const int tid = threadIdx.x;
+  const int dim = op.dim;
+  const int nh = dim - LB;
+  const int nh_loc = op.dim_loc - LB;
+  const uint32_t hmask = (nh >= 32) ? 0xffffffffu : ((1u << nh) - 1u);
+  const uint32_t hbase = (uint32_t)op.rank << nh_loc;
+  const int64_t vbase = (int64_t)op.rank << op.dim_loc;
+  const int64_t ntiles = n >> LB;
+  if (tid == 0) {
+    for (int s = 0; s < NSP; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, CONS / 32);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(afull + s, 1);
+      mbar_init(aempty + s, CONS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  pdl_enter();
+  if (*done) return;
+
+  const int lane = tid & 31;
+  const double2 alpha = make_double2(0.0, -s_k);
+  const double2 one = make_double2(1.0, 0.0);
+  const double g = -op.gamma;
+  double nrm = 0.0;
+
+  if (tid >= CONS) {
+    const int pl = tid - CONS;
+    if (pl < 32 * PROD && (pl & 31) == 0) {
+      // ---------------- producers: partner pairs in row order; producer q
+      // fills the pairs it == q mod PROD, producer 0 also the tile slots
+      const uint32_t q = (uint32_t)pl >> 5;
+      uint32_t s = 0, ph = 0, ti = 0, it = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
+        const uint32_t Hl = (uint32_t)tile, H = hbase | Hl;
+        if (q == 0) {   // acc tile, own tile and (marked runs) the 32 bitmap words
+          const int ab = ti & 1;
+          double2* sb = slotbuf + (size_t)ab * 2 * TILE;
+          mbar_wait(aempty + ab, ((ti >> 1) & 1) ^ 1);
+          mbar_expect_tx(afull + ab, 2 * CHUNK_BYTES + (op.bits ? 128u : 0u));
+          bulk_g2s(sb, acc_in + ((int64_t)Hl << LB), CHUNK_BYTES, afull + ab);
+          bulk_g2s(sb + TILE, tin + ((int64_t)Hl << LB), CHUNK_BYTES, afull + ab);
+          if (op.bits) bulk_g2s(awords + ab * 32, op.bits + ((vbase + (tile << LB)) >> 5), 128u, afull + ab);
+        }
+        uint32_t setm = H, clrm = (~H) & hmask;
+        for (int c = 0; c < nh; c += 2, ++it) {
+          const double2* src[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            int b;
+            if (setm) {
+              b = 31 - __clz(setm);
+              setm ^= 1u << b;
+            } else {
+              b = __ffs(clrm) - 1;
+              clrm ^= 1u << b;
+            }
+            src[h] = b < nh_loc ? tin + ((int64_t)(Hl ^ (1u << b)) << LB) : op.remote[b - nh_loc] + ((int64_t)Hl << LB);
+          }
+          const uint32_t sc = s, pc = ph;
+          if (++s == NSP) {
+            s = 0;
+            ph ^= 1u;
+          }
+          if (PROD > 1 && it % PROD != q) continue;
+          mbar_wait(empty + sc, pc ^ 1);
+          mbar_expect_tx(full + sc, 2 * CHUNK_BYTES);
+          bulk_g2s(ring + (size_t)sc * 2 * TILE, src[0], CHUNK_BYTES, full + sc);
+          bulk_g2s(ring + (size_t)sc * 2 * TILE + TILE, src[1], CHUNK_BYTES, full + sc);
+        }
+      }
+    } else if (pl >= 32 * PROD && op.bits) {
+      // ---------------- fix-up warp (as in hc_stream_kernel)
+      const int fl = pl - 32 * PROD;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint32_t word = __ldg(op.bits + ((vbase + (tile << LB)) >> 5) + fl);
+        unsigned any = __ballot_sync(0xffffffffu, word != 0u);
+        while (any) {
+          const int src = __ffs(any) - 1;
+          any &= any - 1;
+          uint32_t wd = __shfl_sync(0xffffffffu, word, src);
+          while (wd) {
+            const int bit = __ffs(wd) - 1;
+            wd &= wd - 1;
+            const int64_t v = (tile << LB) + src * 32 + bit;
+            const double2 h = hc_marked_row(op, g, tin, v, vbase + v, fl);
+            if (fl == 0) {
+              const double2 t = cmul_np(alpha, h);
+              tout[v] = t;
+              acc_out[v] = cadd(acc_in[v], cmul_np(one, t));
+              nrm = __fma_rn(t.x, t.x, __fma_rn(t.y, t.y, nrm));
+            }
+          }
+        }
+      }
+    }
+  } else {
+    // ---------------- consumers
+    const int m = dim - 1;
+    const int main_end = m - (m % 4);
+    uint32_t offs[VPT][LB / 2];
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+      const uint32_t l = (uint32_t)(tid + j * CONS);
+      uint32_t sm = l, cm = (~l) & (TILE - 1);
+      const int pc = __popc(l);
+#pragma unroll
+      for (int qq = 0; qq < LB; ++qq) {
+        int b;
+        if (qq < pc) {
+          b = 31 - __clz(sm);
+          sm ^= 1u << b;
+        } else {
+          b = __ffs(cm) - 1;
+          cm ^= 1u << b;
+        }
+        const uint32_t off = (l ^ (1u << b)) * (uint32_t)sizeof(double2);
+        if (qq % 2 == 0) offs[j][qq / 2] = off;
+        else offs[j][qq / 2] |= off << 16;
+      }
+    }
+    const uint32_t full_u32 = smem_u32(full), empty_u32 = smem_u32(empty);
+    // C-side partners k >= kt go to the tail (row positions past main_end)
+    const int kt = main_end - LB + 1;
+    uint32_t s = 0, ph = 0, ti = 0;
+    for (uint32_t tile = blockIdx.x; tile < (uint32_t)ntiles; tile += nctaid_x(), ++ti) {
+      const uint32_t H = hbase | (uint32_t)tile;
+      const int hs = __popc(H);
+      double2 x0[VPT], ac[4][VPT];
+#pragma unroll
+      for (int j = 0; j < VPT; ++j) x0[j] = ac[0][j] = ac[1][j] = ac[2][j] = ac[3][j] = make_double2(-0.0, -0.0);
+      auto add_tail = [&](int i, const double2 (&e)[VPT]) {
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+          if (i == main_end) ac[0][j] = cadd(cadd(ac[0][j], ac[1][j]), cadd(ac[2][j], ac[3][j]));
+          ac[0][j] = cadd(ac[0][j], e[j]);
+        }
+      };
+      auto addto = [&](double2 (&acc)[VPT], const double2 (&e)[VPT]) {
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) acc[j] = cadd(acc[j], e[j]);
+      };
+      // the next pair of partner tiles (e: partner 2p, f: 2p + 1)
+      auto take_pair = [&](double2 (&e)[VPT], double2 (&f)[VPT]) {
+        mbar_wait_u32(full_u32 + 8 * s, ph);
+        const double2* c = ring + (size_t)s * 2 * TILE;
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+          e[j] = c[tid + j * CONS];
+          f[j] = c[TILE + tid + j * CONS];
+        }
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+          e[j] = scale_real_z(g, e[j]);
+          f[j] = scale_real_z(g, f[j]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_u32(empty_u32 + 8 * s);
+        if (++s == NSP) {
+          s = 0;
+          ph ^= 1u;
+        }
+      };
+      // partner k = k0 + J (k0 % 4 == 0) before the own tile: slot (J + 3) & 3,
+      // partner 0 is x0 (J is a literal at every call: after inlining the slot
+      // is a fixed register; a generic-lambda form crashes cudafe++ 12.9)
+      auto add_a = [&](int k, int J, const double2 (&e)[VPT]) {
+        if (J == 0 && k == 0)
+          addto(x0, e);
+        else
+          addto(ac[(J + 3) & 3], e);
+      };
+      // after the own tile: slot (J + 1) & 3, or the tail
+      auto add_c = [&](int k, int J, const double2 (&e)[VPT]) {
+        if (k >= kt)
+          add_tail(k + LB - 1, e);
+        else
+          addto(ac[(J + 1) & 3], e);
+      };
+      using I0 = std::integral_constant<int, 0>;
+      using I1 = std::integral_constant<int, 1>;
+      using I2 = std::integral_constant<int, 2>;
+      using I3 = std::integral_constant<int, 3>;
+      const int ab = ti & 1;
+      const double2* sb = slotbuf + (size_t)ab * 2 * TILE;
+      // the own tile, row positions hs .. hs + LB - 1 (after the slot arrived)
+      const char* owncb = reinterpret_cast<const char*>(sb + TILE);
+      auto fold = [&](auto Rc, auto Fc) {
+        constexpr int R = decltype(Rc)::value;
+        constexpr bool FAST = decltype(Fc)::value;
+#pragma unroll
+        for (int qq = 0; qq < LB; ++qq) {
+          double2 e[VPT];
+#pragma unroll
+          for (int j = 0; j < VPT; ++j) {
+            const uint32_t off = (qq % 2 == 0) ? (offs[j][qq / 2] & 0xffffu) : (offs[j][qq / 2] >> 16);
+            e[j] = scale_real_z(g, *reinterpret_cast<const double2*>(owncb + off));
+          }
+          const int a = (R + qq + 3) & 3;
+          if (FAST) {
+            addto(ac[a], e);
+            continue;
+          }
+          const int i = hs + qq - 1;
+          if (i < 0)
+            addto(x0, e);
+          else if (i < main_end)
+            addto(ac[a], e);
+          else
+            add_tail(i, e);
+        }
+      };
+      auto own = [&]() {
+        mbar_wait(afull + ab, (ti >> 1) & 1);
+        if (hs >= 1 && hs + LB - 2 < main_end) {
+          switch (hs & 3) {
+            case 0: fold(I0{}, std::true_type{}); break;
+            case 1: fold(I1{}, std::true_type{}); break;
+            case 2: fold(I2{}, std::true_type{}); break;
+            default: fold(I3{}, std::true_type{}); break;
+          }
+        } else {
+          switch (hs & 3) {
+            case 0: fold(I0{}, std::false_type{}); break;
+            case 1: fold(I1{}, std::false_type{}); break;
+            case 2: fold(I2{}, std::false_type{}); break;
+            default: fold(I3{}, std::false_type{}); break;
+          }
+        }
+      };
+      double2 e[VPT], f[VPT];
+      int k0 = 0;
+      // groups of four partners wholly before the own tile
+      for (; k0 + 4 <= hs; k0 += 4) {
+        take_pair(e, f);
+        add_a(k0, 0, e);
+        add_a(k0, 1, f);
+        take_pair(e, f);
+        add_a(k0, 2, e);
+        add_a(k0, 3, f);
+      }
+      // the group holding the own tile: partners k0 .. min(k0 + 4, nh) - 1,
+      // the own tile after the first r = hs - k0 of them (one call site: the
+      // pending second half of a pair waits in f)
+      {
+        const int r = hs - k0;   // 0..3
+        const bool p0 = k0 < nh, p1 = k0 + 2 < nh;   // pairs present
+        if (r >= 1) {
+          take_pair(e, f);
+          add_a(k0, 0, e);
+        }
+        if (r >= 2) add_a(k0, 1, f);
+        if (r >= 3) {
+          take_pair(e, f);
+          add_a(k0, 2, e);
+        }
+        own();
+        if (r == 1) add_c(k0 + 1, 1, f);
+        if (r == 3) add_c(k0 + 3, 3, f);
+        if (r == 0 && p0) {
+          take_pair(e, f);
+          add_c(k0, 0, e);
+          add_c(k0 + 1, 1, f);
+        }
+        if (r <= 2 && p1) {
+          take_pair(e, f);
+          add_c(k0 + 2, 2, e);
+          add_c(k0 + 3, 3, f);
+        }
+        k0 += 4;
+      }
+      // groups wholly after the own tile: first those clear of the tail
+      for (; k0 + 4 <= kt && k0 + 4 <= nh; k0 += 4) {
+        take_pair(e, f);
+        addto(ac[1], e);
+        addto(ac[2], f);
+        take_pair(e, f);
+        addto(ac[3], e);
+        addto(ac[0], f);
+      }
+      for (; k0 < nh; k0 += 4) {
+        take_pair(e, f);
+        add_c(k0, 0, e);
+        add_c(k0 + 1, 1, f);
+        if (k0 + 2 < nh) {
+          take_pair(e, f);
+          add_c(k0 + 2, 2, e);
+          add_c(k0 + 3, 3, f);
+        }
+      }
+      const double2* ach = sb;
+#pragma unroll
+      for (int j = 0; j < VPT; ++j) {
+        const int64_t v = ((int64_t)tile << LB) + tid + j * CONS;
+        const uint32_t mword = op.bits ? awords[ab * 32 + ((tid + j * CONS) >> 5)] : 0u;
+        if ((mword >> (v & 31)) & 1u) continue;   // marked: the fix-up warp's
+        const double2 rr = (m == main_end) ? cadd(cadd(ac[0][j], ac[1][j]), cadd(ac[2][j], ac[3][j])) : ac[0][j];
+        const double2 t = cmul_np(alpha, cadd(x0[j], rr));
+        tout[v] = t;
+        __stcs(acc_out + v, cadd(ach[tid + j * CONS], cmul_np(one, t)));
+        nrm = __fma_rn(t.x, t.x, __fma_rn(t.y, t.y, nrm));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(aempty + ab);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nrm = __dadd_rn(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
+  if (lane == 0) red[tid >> 5] = nrm;
+  __syncthreads();
+  if (tid == 0) {
+    double r = 0.0;
+    for (int w = 0; w < CONS / 32 + PROD + 1; ++w) r = __dadd_rn(r, red[w]);
+    partial[blockIdx.x] = r;
+  }
+}
+
 // launch one term; returns the number of partials the kernel wrote
 template <int NS, int PROD, int CONS>
 void launch_stream(const HcStream& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
@@ -858,11 +1210,42 @@ void launch_stream(const HcStream& op, cudaStream_t s, int64_t n, const double2*
              ain, acc, s_k, flags, partial);
 }
 
+template <int NSP, int PROD, int CONS>
+void launch_pair(const HcStream& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
+                 const double2* ain, double2* acc, double s_k, const int* flags, double* partial) {
+  static bool configured[256] = {};
+  const int dev = op.device & 255;
+  if (!configured[dev]) {
+    cudaFuncSetAttribute(hc_pair_kernel<NSP, PROD, CONS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)hcs::pair_smem_bytes(NSP));
+    configured[dev] = true;
+  }
+  launch_pdl(hc_pair_kernel<NSP, PROD, CONS>, op.grid, CONS + 32 * PROD + 32, hcs::pair_smem_bytes(NSP), s, op, n,
+             tin, tout, ain, acc, s_k, flags, partial);
+}
+
 int launch_term(const HcStream& op, cudaStream_t s, int64_t n, const double2* tin, double2* tout,
                 const double2* ain, double2* acc, double s_k, const int* flags, double* partial) {
   // QWB_HC_STREAM = CONS/256 * 10000 + NS * 100 + PROD (tuning knob; dim 22,
   // us/term on one box: 21201 105.4, 21202 92.5, 21203 102.5 (96 registers,
   // spills), 21002 94.5; profiles/r02_hc_producers.txt)
+  // paired form (variants < 1000: NSP * 10 + PROD) where the partner count is
+  // even; dim 22 us/term on one box: 52 90.8, 51 91.3, 42 94.0 (21202 92.7);
+  // L2 evict-first / evict-last hints with a persisting set-aside of 0 / 40 /
+  // 64 / 90 MB: 91.2 / 91.0 / 95.3 / 103.3 (profiles/r02_hc_producers.txt)
+  if (op.variant < 1000) {
+    if ((op.dim - hcs::LB) % 2 != 0) {   // odd partner count: the single-chunk ring
+      launch_stream<12, 2, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial);
+      return op.grid;
+    }
+    switch (op.variant) {
+      case 51: launch_pair<5, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+      case 41: launch_pair<4, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+      case 42: launch_pair<4, 2, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+      default: launch_pair<5, 2, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
+    }
+    return op.grid;
+  }
   switch (op.variant) {
     case 21001: launch_stream<10, 1, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
     case 21002: launch_stream<10, 2, 512>(op, s, n, tin, tout, ain, acc, s_k, flags, partial); break;
@@ -1104,7 +1487,7 @@ int hc_stream_base(qwb_ctx* ctx, int dim, int S, double gamma, const uint32_t* b
   static int variant = -1;
   if (variant < 0) {
     const char* e = getenv("QWB_HC_STREAM");
-    variant = (e && *e) ? atoi(e) : 21202;
+    variant = (e && *e) ? atoi(e) : 52;
   }
   const int64_t ntiles = 1LL << (dim - S - hcs::LB);
   *op = HcStream{};
