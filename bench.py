@@ -838,12 +838,13 @@ def measure_extras(q, CO, eng, dev, peak):
                                   "frac": 64 * nv * nterms / dt / 1e9 / peak,
                                   "l2_to_sm_bytes_per_vertex_term": (dim - 10 + 2) * 16,
                                   "l2_to_sm_GBps": (dim - 10 + 2) * 16 * nv * nterms / dt / 1e9,
-                                  "kernel": "hc_stream_kernel (TMA bulk-streamed partner tiles)",
+                                  "kernel": "hc_pair_kernel (TMA bulk-streamed partner tiles, two per stage)",
                                   "note": "64 B/vertex-term = term read + write and acc read-modify-write "
                                           "from HBM; each vertex also needs its 12 high-bit neighbours, "
                                           "streamed from L2 as 16-KB partner tiles ((dim-10+2) x 16 B "
-                                          "per vertex-term over L2->SM): the term is L2-bandwidth and "
-                                          "latency bound, not HBM bound",
+                                          "per vertex-term over L2->SM): the stream misses L2 (the term "
+                                          "is read 13x per term beside 200 MB of other streams) and is "
+                                          "bound there, not by HBM bandwidth (DESIGN.md section 4)",
                                   "inf_norm": op.inf_norm}
     del op, x
     torch.cuda.empty_cache()
