@@ -4,7 +4,7 @@ the CPU oracle, bitwise: the persistent dataflow kernel (QWB_LATTICE_FLOW=2)
 and the per-launch tile kernel (QWB_LATTICE_FLOW=0) on lattices where the
 default would pick the other one, with marked vertices, both shifts, wrap
 tiles narrower than the halo, and a localized start run into the subnormal
-range."""
+range; and the hypercube term kernels' forms (QWB_HC_STREAM)."""
 
 from __future__ import annotations
 
@@ -63,4 +63,39 @@ def test_lattice_launch_forms(flow, nx, ny, steps, shift, localized, marked, tmp
     env = dict(os.environ, QWB_LATTICE_FLOW=flow)
     r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT, str(nx), str(ny), str(steps), shift,
                         "1" if localized else "0", marked], capture_output=True, text=True, env=env, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+HC_SCRIPT = r'''
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2406_08186_b200 as q
+from oracle import qwalk_oracle as O
+dim = int(sys.argv[2])
+marked = tuple(int(v) for v in sys.argv[3].split(",") if v)
+n = 1 << dim
+rng = np.random.default_rng(dim + 1)
+psi = rng.normal(size=n) + 1j * rng.normal(size=n)
+psi /= np.linalg.norm(psi)
+eng = q.init_engine("b200")
+spec = q.CtqwSpec(q.graphs.hypercube(dim), 1.0 / dim, 0.75, frozenset(marked))
+got = q.ctqw.simulate(eng, spec, (0, 2, 1), q.WalkState(q.VertexBasis(n), psi))[-1].amplitudes
+offs, cols = O.hypercube_adjacency(dim)
+ref = O.evolve_state(O.hamiltonian(offs, cols, 1.0 / dim, marked), psi, 0.75)
+bad = int(np.count_nonzero(got != ref))
+print("differ", bad)
+sys.exit(1 if bad else 0)
+'''
+
+
+@pytest.mark.parametrize("variant", ["52", "51", "42", "21202", "21201", "21002"])
+@pytest.mark.parametrize("dim,marked", [(14, "0,777,16383"), (13, "5,8191")])
+def test_hypercube_term_kernel_forms(variant, dim, marked):
+    """The hypercube term kernels forced through QWB_HC_STREAM (paired ring:
+    NSP * 10 + PROD; single ring: CONS/256 * 10000 + NS * 100 + PROD; odd
+    partner counts always take the single ring), bitwise against the oracle."""
+    env = dict(os.environ, QWB_HC_STREAM=variant)
+    r = subprocess.run([sys.executable, "-c", HC_SCRIPT, ROOT, str(dim), marked], capture_output=True, text=True,
+                       env=env, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
