@@ -142,6 +142,20 @@ struct MarkedList {   // up to 8 marked vertex ids; n < 0: more than 8 (use the 
   int x[8], y[8];     // their coordinates (host-computed)
 };
 
+// Marked vertex `lane` of the list in registers (lanes 0..7; static indices:
+// the list stays in the parameter space), so a tile's "does my region hold a
+// marked vertex" test is one check per lane and a warp vote.
+struct MarkLane {
+  int x, y;
+};
+__device__ __forceinline__ MarkLane mark_lane(const MarkedList& mk, int lane) {
+  MarkLane ml{-1, -1};
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (lane == j) ml = MarkLane{mk.x[j], mk.y[j]};
+  return ml;
+}
+
 // p of a traced vertex from its level-t amplitudes a[0..3] (planes D, L, R,
 // U; sc undoes the doubled-space scale): reference slot order, numpy |z|^2,
 // row sum.
@@ -415,6 +429,58 @@ __device__ __noinline__ void tile_exact(int nx, int ny, int64_t n, int lrows, in
   }
 }
 
+// A tile whose region holds a marked vertex (rare: a few tiles per launch),
+// doubled space, region reloaded from `in` (L2 loads, as tile_exact).  Out of
+// line: inlined, the marked slot path changed the code of the whole MARKED
+// kernel and every interior tile ran 6.5 % slower (4096^2: 94.5 vs 88.8
+// us/step, profiles/r02_marked_variant.txt).  m: the threads' tiny-input flags
+// from the stage, tested against key on the first step's barrier.
+template <int SHIFT, int T, int BY, int V, bool SLAB>
+__device__ __noinline__ bool tile_marked(int nx, int ny, int64_t n, int lrows, int x0, int y0, int lyb,
+                                         int rows_left, unsigned m, unsigned key, const double2* __restrict__ in,
+                                         const uint32_t* __restrict__ bits, double2* xD, double2* xU,
+                                         double2* __restrict__ out, int* sticky) {
+  using S = TbShape<BY, V>;
+  constexpr int OX = S::RX - 2 * T, OY = S::RY - 2 * T;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  const int gx = wrapc(x0 - T + tx, nx);
+  int gy[V];
+  double2 vD[V], vL[V], vR[V], vU[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    gy[j] = wrapc(y0 - T + ty * V + j, ny);
+    const int ly = lyb - T + ty * V + j;
+    const bool ok = !SLAB || (ly >= 0 && ly < lrows);
+    const int64_t w = (int64_t)(SLAB ? (ok ? ly : 0) : wrapc(ly, ny)) * nx + gx;
+    const double2 z = make_double2(0.0, 0.0);
+    vD[j] = ok ? __ldcg(in + w) : z;
+    vL[j] = ok ? __ldcg(in + n + w) : z;
+    vR[j] = ok ? __ldcg(in + 2 * n + w) : z;
+    vU[j] = ok ? __ldcg(in + 3 * n + w) : z;
+  }
+  const bool tiny = tile_steps<SHIFT, true, T, BY, V, false, false>(nx, ny, gx, gy, m, key, bits, vD, vL, vR, vU,
+                                                                   xD, xU, tid, ty, NoHook{});
+  if (tiny) {
+    if (sticky && tid == 0) atomicOr(sticky, 1);
+    tile_exact<SHIFT, true, T, BY, V, SLAB>(nx, ny, n, lrows, x0, y0, lyb, rows_left, false, in, bits, xD, xU, out);
+    return true;
+  }
+  constexpr double sc = 1.0 / (double)(1 << T);
+  const bool col_ok = tx >= T && tx < T + OX && x0 + tx - T < nx;
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    const int ly = ty * V + j;
+    if (col_ok && ly >= T && ly < T + OY && ly - T < rows_left) {
+      const int64_t w = (int64_t)(lyb - T + ly) * nx + gx;
+      __stcs(out + w, make_double2(__dmul_rn(vD[j].x, sc), __dmul_rn(vD[j].y, sc)));
+      __stcs(out + n + w, make_double2(__dmul_rn(vL[j].x, sc), __dmul_rn(vL[j].y, sc)));
+      __stcs(out + 2 * n + w, make_double2(__dmul_rn(vR[j].x, sc), __dmul_rn(vR[j].y, sc)));
+      __stcs(out + 3 * n + w, make_double2(__dmul_rn(vU[j].x, sc), __dmul_rn(vU[j].y, sc)));
+    }
+  }
+  return false;
+}
+
 // Steps + store of one tile whose registers are loaded.  (x0, y0): global
 // column / unwrapped global row of its first owned vertex; lyb: local buffer
 // row of that row; rows_left: owned rows from y0 to the end of the launch's
@@ -432,7 +498,8 @@ __device__ __forceinline__ bool tile_run(int nx, int ny, int64_t n, int lrows, i
                                          const uint32_t* __restrict__ bits, const MarkedList& mk,
                                          double2 (&vD)[V], double2 (&vL)[V], double2 (&vR)[V], double2 (&vU)[V],
                                          double2* xD, double2* xU, double2* __restrict__ out, int tx, int ty,
-                                         int tid, const F& after0, int* sticky = nullptr) {
+                                         int tid, const F& after0, int* sticky = nullptr,
+                                         MarkLane ml = MarkLane{-1, -1}) {
   using S = TbShape<BY, V>;
   constexpr int OX = S::RX - 2 * T, OY = S::RY - 2 * T;
   const int gx = wrapc(x0 - T + tx, nx);
@@ -441,16 +508,14 @@ __device__ __forceinline__ bool tile_run(int nx, int ny, int64_t n, int lrows, i
   for (int j = 0; j < V; ++j) gy[j] = wrapc(y0 - T + ty * V + j, ny);
   // regions with no torus edge row and no marked vertex: one formula
   bool interior = y0 - T >= 1 && y0 - T + S::RY - 1 <= ny - 2;
-  if (MARKED && interior) {
-    if (mk.n < 0) {
-      interior = false;   // too many marked vertices for the list: general path
-    } else {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int dx = wrapc(mk.x[k] - (x0 - T) + nx, nx), dy = mk.y[k] - (y0 - T);
-        interior &= (k >= mk.n) || !(dx < S::RX && dy >= 0 && dy < S::RY);
-      }
-    }
+  bool has_marked = false;   // the region holds a marked vertex: out-of-line path
+  if (MARKED) {
+    // lane k tests marked vertex k: offsets from the region's first column /
+    // row modulo the torus (arguments within one period of [0, n): x0 in
+    // [0, nx), y0 - T within a slab's ghost rows of [0, ny))
+    const int dx = wrapc(ml.x - (x0 - T), nx), dy = wrapc(ml.y - (y0 - T), ny);
+    has_marked = mk.n < 0 || __any_sync(0xffffffffu, tx < mk.n && dx < S::RX && dy < S::RY);
+    interior &= !has_marked;
   }
   if (all_exact) {   // a run that met tiny amplitudes: numpy's arithmetic from the start
     __syncthreads();   // after0 reads what the flow kernel's polling warp decided just before
@@ -459,11 +524,17 @@ __device__ __forceinline__ bool tile_run(int nx, int ny, int64_t n, int lrows, i
                                               out);
     return true;
   }
+  if (MARKED && has_marked) {
+    __syncthreads();   // as above
+    after0();
+    return tile_marked<SHIFT, T, BY, V, SLAB>(nx, ny, n, lrows, x0, y0, lyb, rows_left, m, key, in, bits, xD, xU,
+                                              out, sticky);
+  }
   const bool tiny =
       interior ? tile_steps<SHIFT, false, T, BY, V, true, false>(nx, ny, gx, gy, m, key, bits, vD, vL, vR, vU, xD,
                                                                  xU, tid, ty, after0)
-               : tile_steps<SHIFT, MARKED, T, BY, V, false, false>(nx, ny, gx, gy, m, key, bits, vD, vL, vR, vU, xD,
-                                                                   xU, tid, ty, after0);
+               : tile_steps<SHIFT, false, T, BY, V, false, false>(nx, ny, gx, gy, m, key, bits, vD, vL, vR, vU, xD,
+                                                                  xU, tid, ty, after0);
   if (tiny) {
     if (sticky && tid == 0) atomicOr(sticky, 1);
     tile_exact<SHIFT, MARKED, T, BY, V, SLAB>(nx, ny, n, lrows, x0, y0, lyb, rows_left, interior, in, bits, xD, xU,
@@ -503,6 +574,7 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
   double2* xU = xD + 2 * S::NT;                // [2][BY][32] O_U of each thread's highest row
   uint64_t* tbar = reinterpret_cast<uint64_t*>(xU + 2 * S::NT);   // [2] stage barriers
   const int tx = threadIdx.x, ty = threadIdx.y;
+  const MarkLane ml = MARKED ? mark_lane(mk, tx) : MarkLane{-1, -1};
   const int tid = ty * 32 + tx;
   if (!SLAB) geo = TbGeo{ny, 0, ny, 0, 1};   // compile-time constants for the torus
   if (tid == 0) {
@@ -590,7 +662,7 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
     ptile += gridDim.x;
     tile_run<SHIFT, MARKED, T, BY, V, SLAB>(nx, ny, n, geo.lrows, x0, y0, lyb, geo.nown - trow_now * OY, m, key,
                                             all_exact, in, bits, mk, vD, vL, vR, vU, xD, xU, out, tx, ty, tid,
-                                            NoHook{}, sticky);
+                                            NoHook{}, sticky, ml);
 #ifdef QWB_EXP_TIMING
     DBG_T(t_d);
     if (tid == 0) {
@@ -648,6 +720,7 @@ lattice_flow_kernel(int nx, int ny, FlowArgs fa, const uint32_t* __restrict__ bi
   // iteration it's item inherits the subnormal flag (from its dependencies)
   int* shw = reinterpret_cast<int*>(tbar + 2);
   const int tx = threadIdx.x, ty = threadIdx.y;
+  const MarkLane ml = MARKED ? mark_lane(mk, tx) : MarkLane{-1, -1};
   const int tid = ty * 32 + tx;
   const int ntiles = tiles_x * tiles_y;
   const int64_t n = (int64_t)nx * ny;
@@ -804,7 +877,7 @@ lattice_flow_kernel(int nx, int ny, FlowArgs fa, const uint32_t* __restrict__ bi
     const bool exact_used =
         tile_run<SHIFT, MARKED, T, BY, V, false>(nx, ny, n, ny, cur.c * OX, tr * OY, tr * OY, ny - tr * OY, m,
                                                  check ? qwb::kTinyKeyPeriodic : 0u, all_exact, in, bits, mk, vD, vL,
-                                                 vR, vU, xD, xU, out, tx, ty, tid, after0);
+                                                 vR, vU, xD, xU, out, tx, ty, tid, after0, nullptr, ml);
 #ifdef QWB_EXP_TIMING
     DBG_T(t_d);
     if (tid == 0) {

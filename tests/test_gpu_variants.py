@@ -58,6 +58,8 @@ sys.exit(1 if bad else 0)
     (1018, 290, 33, "flipflop", False, "0,1017,294000"),            # last tile column 10 wide, row 10 high
     (290, 1022, 26, "persistent", False, "145"),                    # last tile column 2 wide (< T)
     (2304, 256, 1100, "flipflop", True, ""),                        # front into subnormals
+    (1024, 1024, 40, "flipflop", False, "525311,308221"),           # marked at x = nx - 1 and nx - 3, interior
+                                                                    # rows: halo columns of the x0 = 0 tiles
 ])
 def test_lattice_launch_forms(flow, nx, ny, steps, shift, localized, marked, tmp_path):
     env = dict(os.environ, QWB_LATTICE_FLOW=flow)
