@@ -101,3 +101,31 @@ def test_hypercube_term_kernel_forms(variant, dim, marked):
     r = subprocess.run([sys.executable, "-c", HC_SCRIPT, ROOT, str(dim), marked], capture_output=True, text=True,
                        env=env, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def _fuzz_case(seed):
+    """A random torus, step count, shift and marked set (biased to the torus
+    edges, the halo columns that wrap, and to more than 8 vertices: the
+    bitmap path)."""
+    import numpy as np
+    rng = np.random.default_rng(1000 + seed)
+    nx, ny = (int(v) for v in rng.integers(64, 600, size=2))
+    steps = int(rng.integers(1, 40))
+    shift = ("flipflop", "persistent")[seed % 2]
+    k = int(rng.choice([0, 1, 3, 9]))
+    xs = [int(v) for v in rng.choice([0, 1, 5, nx - 1, nx - 3, nx - 6, nx // 2, int(rng.integers(0, nx))], size=k)]
+    ys = [int(v) for v in rng.choice([0, 1, 7, ny - 1, ny - 2, ny // 2, int(rng.integers(0, ny))], size=k)]
+    marked = sorted({y * nx + x for x, y in zip(xs, ys)})
+    return nx, ny, steps, shift, ",".join(str(v) for v in marked)
+
+
+@pytest.mark.parametrize("form", ["launch", "flow"])
+@pytest.mark.parametrize("seed", range(int(os.environ.get("QWB_FUZZ_CASES", "8"))))
+def test_lattice_fuzz(seed, form):
+    """Random tori, step counts, shifts and marked sets through the lattice
+    kernels, bitwise against the oracle."""
+    nx, ny, steps, shift, marked = _fuzz_case(seed)
+    env = dict(os.environ, QWB_LATTICE_FLOW={"launch": "0", "flow": "2"}[form])
+    r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT, str(nx), str(ny), str(steps), shift, "0", marked],
+                       capture_output=True, text=True, env=env, timeout=900)
+    assert r.returncode == 0, f"{nx}x{ny} {steps} {shift} marked {marked}: " + r.stdout + r.stderr
