@@ -842,9 +842,9 @@ def measure_extras(q, CO, eng, dev, peak):
                                   "note": "64 B/vertex-term = term read + write and acc read-modify-write "
                                           "from HBM; each vertex also needs its 12 high-bit neighbours, "
                                           "streamed from L2 as 16-KB partner tiles ((dim-10+2) x 16 B "
-                                          "per vertex-term over L2->SM): the stream misses L2 (the term "
-                                          "is read 13x per term beside 200 MB of other streams) and is "
-                                          "bound there, not by HBM bandwidth (DESIGN.md section 4)",
+                                          "per vertex-term over L2->SM); the kernel is bound by its "
+                                          "consumer warps' latency chain, not by HBM or L2 bandwidth "
+                                          "(DESIGN.md section 4)",
                                   "inf_norm": op.inf_norm}
     del op, x
     torch.cuda.empty_cache()
