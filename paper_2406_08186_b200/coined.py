@@ -382,7 +382,9 @@ def search_trace(engine: Engine, spec: CoinedSpec, steps: int, psi0: WalkState,
     every = distribution_every if distribution_every > 0 else steps + 1
     # saved distributions download beside the steps that follow them
     keys = list(range(every, steps + 1, every))
-    pipe = SnapshotPipe(engine, g.n, max(2, len(keys)), dtype=torch.float64)
+    # pageable results through bounce buffers: 4096 steps between distributions
+    # leave ample time for the host copies, and nothing is page-locked
+    pipe = SnapshotPipe(engine, g.n, max(2, len(keys)), dtype=torch.float64, pinned=False)
     while done < steps:
         chunk = min(steps - done, every - (done % every))
         r.advance(chunk, trace[done:], marked)
