@@ -353,8 +353,8 @@ hc_pos_kernel(HcPos<MAXD> op, int64_t n, const double2* __restrict__ tin, double
 // and the consumer threads fold each stage into the numpy pairwise
 // accumulators of their vertices in order: every global read is a 16-KB bulk
 // transfer, no gather, no long-scoreboard stall on the compute warps.
-// Vertices of marked rows (diagonal entry, row length dim+1) are recomputed by
-// the generic ordered row after the stream (rare).
+// Vertices of marked rows (diagonal entry, row length dim+1) are computed by a
+// dedicated fix-up warp (hc_marked_row); the consumers skip them.
 // ---------------------------------------------------------------------------
 namespace hcs {
 constexpr int LB = 10;                     // low bits per tile
