@@ -89,6 +89,16 @@ __device__ __forceinline__ void acquire_for_async() {
 
 #ifdef QWB_EXP_TIMING
 __device__ unsigned long long g_dbg[2][8];   // [kernel: 0 tile, 1 flow][slot]
+// launch timeline (tools/r02_timeline.py): per launch and CTA, globaltimer at
+// entry, after the grid-dependency wait, when the first tile's stage is ready,
+// at exit
+__device__ unsigned long long g_tl[64][160][4];
+__device__ unsigned int g_ctas;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ unsigned long long dbg_clock() { return clock64(); }
 #define DBG_T(var) const unsigned long long var = dbg_clock()
 #define DBG_ADD(k, slot, v) atomicAdd(&g_dbg[k][slot], (unsigned long long)(v))
@@ -566,6 +576,9 @@ __global__ void __launch_bounds__(32 * BY, 1)
 lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, double2* __restrict__ out,
                   const uint32_t* __restrict__ bits, MarkedList mk, int tiles_x, int ntiles, int tile0,
                   const __grid_constant__ CUtensorMap imap, int use_tma, unsigned key, int* sticky) {
+#ifdef QWB_EXP_TIMING
+  const unsigned long long tl0 = gtime();
+#endif
   using S = TbShape<BY, V>;
   constexpr int OX = S::RX - 2 * T, OY = S::RY - 2 * T;   // exact (owned) block
   extern __shared__ __align__(128) double2 sm[];
@@ -615,6 +628,12 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
   // launch's last tiles; its output (this launch's input) is visible after the
   // wait (a no-op when launched without the PDL attribute)
   qwb::pdl_wait();
+#ifdef QWB_EXP_TIMING
+  const unsigned long long tl1 = gtime();
+  unsigned long long tl2 = 0;
+  unsigned lid = 0;
+  if (threadIdx.x == 0 && threadIdx.y == 0) lid = atomicAdd(&g_ctas, 1u) / gridDim.x;
+#endif
   int tile = blockIdx.x + tile0;   // tile0 > 0: a launch over tiles [tile0, ntiles) only
   if (tile >= ntiles) return;
   // key != 0: test the tiles' inputs (and raise *sticky on a hit); key == 0:
@@ -652,6 +671,9 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
     }
     DBG_T(t_b);
     const unsigned m = stage_to_regs<S, V>(stage0 + (size_t)k * 4 * S::REG, tx, ty, vD, vL, vR, vU, check);
+#ifdef QWB_EXP_TIMING
+    if (it == 0) tl2 = gtime();
+#endif
     __syncthreads();   // stage k consumed
     DBG_T(t_c);
     if (ptile < ntiles)
@@ -674,6 +696,14 @@ lattice_tb_kernel(int nx, int ny, TbGeo geo, const double2* __restrict__ in, dou
     if (tid == 32 * 7) DBG_ADD(0, 4, dbg_clock() - t_c);   // a storing warp
 #endif
   }
+#ifdef QWB_EXP_TIMING
+  if (threadIdx.x == 0 && threadIdx.y == 0 && lid < 64 && blockIdx.x < 160) {
+    g_tl[lid][blockIdx.x][0] = tl0;
+    g_tl[lid][blockIdx.x][1] = tl1;
+    g_tl[lid][blockIdx.x][2] = tl2;
+    g_tl[lid][blockIdx.x][3] = gtime();
+  }
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -1248,6 +1278,14 @@ extern "C" int qwb_lattice_fused_depth(int64_t nx, int64_t ny, int64_t n_marked,
 }
 
 #ifdef QWB_EXP_TIMING
+extern "C" int qwb_exp_timeline(unsigned long long* out_host, int reset) {
+  cudaMemcpyFromSymbol(out_host, g_tl, sizeof(g_tl));
+  if (reset) {
+    unsigned int z = 0;
+    cudaMemcpyToSymbol(g_ctas, &z, sizeof(z));
+  }
+  return 0;
+}
 extern "C" int qwb_exp_dbg(unsigned long long* out_host, int reset) {
   cudaMemcpyFromSymbol(out_host, g_dbg, sizeof(g_dbg));
   if (reset) {
